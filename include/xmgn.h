@@ -1,0 +1,162 @@
+/* xmgn.h -- C-ABI of the B200-native X-MeshGraphNet processor hot path.
+ *
+ * Method: X-MeshGraphNet (arXiv 2411.17164).  The processor is L message-passing
+ * layers (Sec. II-C, Eq. 4) run over halo-padded partitions of
+ * a merged multi-scale kNN graph (Sec. III-A, 187-194 Sec. III-C).
+ * Layer l, read per BASELINE.json north_star and SURVEY.md §8(c):
+ *     e'_k = e_k + LN_e(MLP_e([e_k | h_src(k) | h_dst(k)]))        (Eq. 1)
+ *     a_i  = sum_{k : dst(k) = i} e'_k      (CSR order)              (Eq. 2)
+ *     h'_i = h_i + LN_n(MLP_n([h_i | a_i]))                          (Eq. 3)
+ * MLP = Linear -> SiLU -> (Linear -> SiLU)^(m-1) -> Linear (SiLU per PAPER.md:234),
+ * LN = per-row LayerNorm with affine gamma/beta, eps = cfg.ln_eps, biased variance.
+ * Loss seam: the caller supplies dL/dh^L for OWNED rows only; halo rows are
+ * dropped from the loss.  Parameter gradients of all partitions
+ * are summed -- plain sum, not a mean.
+ *
+ * Conventions
+ *  - Every call returns xmgn_status; on failure xmgn_last_error() returns a
+ *    thread-local, library-owned message naming the call, array and index
+ *    (valid until the next call on that thread).
+ *  - Host arrays in descriptors are caller-owned and only read during the call.
+ *  - Device pointers (params, features, gradients) are caller-owned CUDA
+ *    allocations on the graph's device; fwd/bwd/reduce enqueue on `stream`
+ *    (a cudaStream_t, NULL = legacy default stream) and return immediately;
+ *    device faults surface at the next synchronising call.
+ *  - One host thread per workspace at a time.
+ *  - Local row order of a partition is ring-major: ring 0 (owned, ascending
+ *    global id), then halo ring 1..depth (ascending global id inside a ring).
+ *    Owned rows are therefore the prefix [0, n_owned).  Local in-edges of a row
+ *    keep the global CSR order.  (SURVEY §2.2 D5.)
+ *  - Parameters: one flat FP32 vector, per layer l = 0..L-1
+ *      edge block: W1[3H,H] (row blocks e, h_src, h_dst), b1[H],
+ *                  W_j[H,H], b_j[H] for j = 2..m+1, gamma[H], beta[H]
+ *      node block: W1[2H,H] (row blocks h, agg), b1[H], W_j, b_j, gamma, beta
+ *    with y = x W + b, W stored [in, out] row-major.
+ *    Count = L*((5+2m)H^2 + (2m+6)H).
+ */
+#ifndef XMGN_H
+#define XMGN_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  XMGN_OK = 0,
+  XMGN_EINVAL = 1,     /* malformed argument / graph (message names array + index)      */
+  XMGN_EHALO = 2,      /* halo_depth < layers, or an owned node's L-hop ball not local   */
+  XMGN_ESTATE = 3,     /* call out of order (bwd without matching fwd, ...)               */
+  XMGN_ENOMEM = 4,     /* device or host allocation failed                                 */
+  XMGN_ECUDA = 5,      /* CUDA runtime error (message carries the runtime string)          */
+  XMGN_ENCCL = 6,      /* NCCL error                                                       */
+  XMGN_ENONFINITE = 7, /* non-finite value detected by xmgn_check_finite      */
+  XMGN_EUNSUPPORTED = 8 /* configuration the kernels are not built for (e.g. H)           */
+} xmgn_status;
+
+const char* xmgn_last_error(void);
+const char* xmgn_version(void);
+
+/* ------------------------------------------------------------------ graph
+ * Global graph in CSR by destination: row i lists the
+ * sources j of edges (j -> i), strictly ascending; no self-loops, no duplicates;
+ * the graph must be symmetric ((j->i) present iff (i->j) present).
+ * owned: n_parts disjoint ascending lists covering [0, n_nodes).
+ * halo:  per partition the nodes at undirected hop distance 1..halo_depth from
+ *        its owned set, ordered by (ring, id), with their ring in halo_ring.
+ * Validation: EINVAL for any malformed array; EHALO if halo_depth is smaller
+ * than the layer count later used, or if the halo lists are not exactly the BFS
+ * rings (checked by an independent BFS).  All arrays are copied; the device
+ * copies are owned by the returned handle.                                      */
+typedef struct {
+  int64_t n_nodes, n_edges;
+  const int64_t* csr_offsets;   /* [n_nodes+1]                               */
+  const int64_t* csr_sources;   /* [n_edges]                                 */
+  int32_t n_parts, halo_depth;
+  const int64_t* owned_offsets; /* [n_parts+1] into owned                    */
+  const int64_t* owned;         /* [n_nodes]                                 */
+  const int64_t* halo_offsets;  /* [n_parts+1] into halo                     */
+  const int64_t* halo;          /* concatenated halo lists                   */
+  const int32_t* halo_ring;     /* ring (1..halo_depth) of each halo entry    */
+} xmgn_graph_desc;
+
+typedef struct xmgn_graph xmgn_graph;
+typedef struct xmgn_workspace xmgn_workspace;
+typedef struct xmgn_comm xmgn_comm;
+
+typedef struct {
+  int64_t n_owned, n_local, e_local;
+  int32_t depth;
+  int64_t ring_nodes[65]; /* ring_nodes[r] = #local nodes with ring < r (r = 0..depth+1) */
+  int64_t ring_edges[65]; /* ring_edges[r] = #local edges whose dst ring < r             */
+} xmgn_part_info;
+
+xmgn_status xmgn_load_graph(const xmgn_graph_desc* desc, int cuda_device, xmgn_graph** out);
+xmgn_status xmgn_part_info_get(const xmgn_graph* g, int part, xmgn_part_info* out);
+/* Host copies of a partition's local arrays (caller-allocated, sizes from
+ * part_info): local_node_gid[n_local], local_offsets[n_local+1],
+ * local_src_lid[e_local], local_edge_gid[e_local], rev[e_local] (index of the
+ * reverse local edge).  Any pointer may be NULL.  For bit-exact tests.        */
+xmgn_status xmgn_export_part(const xmgn_graph* g, int part, int64_t* local_node_gid, int64_t* local_offsets,
+                             int64_t* local_src_lid, int64_t* local_edge_gid, int64_t* rev);
+void xmgn_free_graph(xmgn_graph* g);
+
+/* ------------------------------------------------------------------ model
+ * precision: XMGN_PREC_BF16 -- BF16 tensor-core operands, FP32 accumulate,
+ *            FP32 residual streams / LN / SiLU / aggregation (PAPER.md:234 AMP).
+ *            XMGN_PREC_FP32_CHECK -- every GEMM operand split hi+lo in BF16 and
+ *            multiplied as hi*hi + lo*hi + hi*lo (FP32-class products) for the
+ *            1e-4 check mode (north_star); H <= 256 only.
+ * mlp_hidden_layers m in {1, 2}; hidden H in {128, 256, 512}.                  */
+enum { XMGN_PREC_BF16 = 0, XMGN_PREC_FP32_CHECK = 1 };
+typedef struct {
+  int32_t hidden, layers, mlp_hidden_layers, precision;
+  float ln_eps;
+} xmgn_model_cfg;
+
+size_t xmgn_param_count(const xmgn_model_cfg* cfg);
+/* Workspace for one GPU: per-layer BF16 checkpoints, scratch and gradient
+ * streams sized for the graph's largest partition; reused across that GPU's
+ * sequential partitions.  Requires cfg->layers <= halo depth (else EHALO).    */
+xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_model_cfg* cfg, xmgn_workspace** out);
+size_t xmgn_workspace_bytes(const xmgn_workspace* ws);
+void xmgn_workspace_free(xmgn_workspace* ws);
+
+/* Forward of partition `part`: params [param_count] FP32,
+ * h0 [n_local,H] FP32, e0 [e_local,H] FP32 (local order) -> h_out [n_owned,H]
+ * FP32 = h^L of the owned rows.  Keeps per-layer checkpoints in the workspace
+ * (activation checkpointing) for xmgn_processor_bwd.           */
+xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const float* params, const float* h0,
+                               const float* e0, float* h_out, void* stream);
+/* Backward of the most recent fwd on this workspace (else ESTATE):
+ * grad_h_out [n_owned,H] = dL/dh^L on owned rows; grad_params [param_count]
+ * is ACCUMULATED (+=) so partitions sum in call order;
+ * grad_h0 [n_local,H] / grad_e0 [e_local,H] are overwritten (may be NULL).   */
+xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const float* params, const float* grad_h_out,
+                               float* grad_params, float* grad_h0, float* grad_e0, void* stream);
+/* Synchronises `stream` and returns ENONFINITE if any of n FP32 values is not
+ * finite.                                                  */
+xmgn_status xmgn_check_finite(const float* dev, size_t n, void* stream);
+
+/* ------------------------------------------------------------------ gradient aggregation
+ * One NCCL communicator per process/GPU (one process per GPU).  The unique id
+ * is created on rank 0 and broadcast by the caller (e.g. torch.distributed).
+ * xmgn_grad_reduce: in-place SUM all-reduce of `count` FP32 values on `stream`
+ * ("gradients from all partitions are aggregated").            */
+xmgn_status xmgn_comm_unique_id(uint8_t id[128]);
+xmgn_status xmgn_comm_init(const uint8_t id[128], int nranks, int rank, int cuda_device, xmgn_comm** out);
+xmgn_status xmgn_grad_reduce(xmgn_comm* comm, float* grad_params, size_t count, void* stream);
+void xmgn_comm_destroy(xmgn_comm* comm);
+
+/* ------------------------------------------------------------------ diagnostics
+ * C[M,N] FP32 = A * B^T on tcgen05 with A [M,K] (a_mn_major=0) or [K,M] (=1)
+ * and B [N,K] (b_mn_major=0) or [K,N] (=1), BF16 device arrays; K % 64 == 0,
+ * N in {64,128,256}.  Exercises the descriptor conventions of every kernel.  */
+xmgn_status xmgn_selftest_gemm(int M, int N, int K, int a_mn_major, int b_mn_major, const void* A,
+                               const void* B, float* C, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XMGN_H */

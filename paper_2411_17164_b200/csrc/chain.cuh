@@ -1,0 +1,571 @@
+// The fused per-tile GEMM-chain kernel: every MLP of the processor (forward,
+// recompute, dgrad) runs through it.
+//
+// One persistent CTA per SM walks 128-row tiles.  For each tile it executes a
+// short PROGRAM of steps; step s computes acc[128, N] = A_s[128, K_s] * B_s^T
+// on tcgen05 (BF16 operands, FP32 accumulator in TMEM, N = H <= 512 columns)
+// followed by a fused epilogue.  A_s is either
+//   * A_TMA: rows of one or two global BF16 tensors (concatenated along K),
+//     streamed by TMA through the A ring, or
+//   * A_ACT: the previous step's epilogue output kept on chip in the ACT tile
+//     (128 x H BF16 in shared memory, 128-byte-swizzled K-major) -- so an
+//     MLP's hidden activations never touch HBM.
+// B_s (weights, K-major = W^T or W) is streamed by TMA through the B ring.
+//
+// Warp roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer
+// (one elected lane), warp 2 = TMEM allocator, warps 4..7 = epilogue (thread
+// = tile row = TMEM lane).  The A ring aliases the ACT tile: a program never
+// needs both at once (A_TMA steps only start after the previous step's MMAs
+// retired, and an epilogue that writes ACT is always followed by an A_ACT step).
+//
+// FP32 check mode (SPLIT): every operand is carried as hi + lo BF16 and each
+// k-step issues hi*hi + lo*hi + hi*lo (FP32-class products, north_star's
+// "FP32 check mode").
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda.h>
+#include "tc.cuh"
+
+namespace xmgn {
+
+enum : int { A_TMA = 0, A_ACT = 1 };
+enum : int {
+  EPI_SILU = 0,    // v = acc + b (+ P[src] + P[dst]) -> SiLU -> ACT (+ scratch A, S')
+  EPI_LN_FWD = 1,  // v = acc + b -> LN -> out = res + y (fp32 + bf16 [+ ACT])
+  EPI_STORE = 2,   // out[:, col0 + c] = acc
+  EPI_LN_BWD = 3,  // recompute LN, dY = G (+ Ga[dst]) -> dZ -> ACT + scratch; dgamma, dbeta, db
+  EPI_DSILU = 4,   // dZ = acc * S' -> ACT + scratch; db
+  EPI_ADD = 5      // out = (r < valid ? in : 0) (+ Ga[dst]) + acc
+};
+enum : int {
+  EF_GATHER_P = 1,     // EPI_SILU: add P[src][c] + P[dst][H + c]
+  EF_STORE_A = 2,      // EPI_SILU: scratch A = SiLU(v)
+  EF_STORE_S = 4,      // EPI_SILU: scratch S = SiLU'(v)
+  EF_WRITE_ACT = 8,    // EPI_LN_FWD: also write the BF16 output into ACT
+  EF_GATHER_G = 16,    // EPI_LN_BWD / EPI_ADD: add Ga[dst][c]
+  EF_STORE_BF = 32     // EPI_LN_FWD: write bf16 output (checkpoint)
+};
+
+enum : int {
+  CTL_WAIT_ACT = 1,      // A_ACT step whose A was just written by the previous epilogue
+  CTL_NEED_ACT_FREE = 2  // A_TMA step that must wait until no MMA reads ACT (A ring aliases ACT)
+};
+
+struct Step {
+  int a_src, a_map0, a_map1, a_ksplit;  // A source; tensor-map slots (hi; lo = slot+1 in SPLIT)
+  int ctl;                               // CTL_* (derived on the host from the program)
+  int b_map, b_row0, K;                  // weight map slot, first weight row, reduction length
+  int epi, flags, col0, vec0;            // epilogue op, flags, output column offset, colsum vector
+  int valid_in;                          // rows of f_in that are valid (EPI_LN_BWD / EPI_ADD)
+  const float* bias;
+  const float* gamma;
+  const float* beta;
+  const float* f_in;    // residual input / incoming gradient  [rows][ld_in]
+  float* f_out;         // fp32 output [rows][ld_out]
+  int ld_in, ld_out;
+  const float* gather;  // P [N][2H] (EF_GATHER_P) or Ga [N][H] (EF_GATHER_G)
+  __nv_bfloat16* bf_out;     // bf16 row output hi [rows][H]; lo at bf_out + bf_lo_off
+  __nv_bfloat16* scr_a;      // scratch SiLU(v)
+  __nv_bfloat16* scr_s;      // scratch SiLU'(v) (written by EPI_SILU, read by EPI_DSILU)
+  __nv_bfloat16* scr_z;      // scratch dZ
+  long long lo_off;          // element offset of the lo half of the scratch buffers (SPLIT)
+  long long bf_lo;           // element offset of the lo half of bf_out (SPLIT)
+};
+
+constexpr int MAX_STEPS = 8;
+constexpr int MAX_MAPS = 8;
+constexpr int NV_MAX = 5;  // column-sum vectors per kernel
+
+struct ChainParams {
+  CUtensorMap maps[MAX_MAPS];
+  Step steps[MAX_STEPS];
+  int n_steps;
+  int M;              // rows
+  const int* src;     // [M] source local id of each edge row (edge programs)
+  const int* dst;     // [M] destination local id
+  float* colsum;      // [gridDim.x][4][NV_MAX][H] partial column sums (backward)
+  float eps;          // LayerNorm epsilon
+};
+
+template <int H, bool SPLIT>
+struct ChainCfg {
+  static constexpr int F = SPLIT ? 2 : 1;
+  static constexpr int NB = H < 256 ? H : 256;                 // N rows per B slot / MMA
+  static constexpr uint32_t ACT_HALF = 128u * H * 2u;          // one BF16 copy of the ACT tile
+  static constexpr uint32_t ACT_BYTES = F * ACT_HALF;
+  static constexpr uint32_t A_SLOT_HALF = 128u * 64u * 2u;     // 16 KiB
+  static constexpr uint32_t A_SLOT = F * A_SLOT_HALF;
+  static constexpr int SA = ACT_BYTES / A_SLOT;
+  static constexpr uint32_t B_SLOT_HALF = NB * 128u;
+  static constexpr uint32_t B_SLOT = F * B_SLOT_HALF;
+  static constexpr uint32_t SMEM_LIMIT = 227u * 1024u;
+  static constexpr int SB_FIT = (int)((SMEM_LIMIT - 2048u - ACT_BYTES) / B_SLOT);
+  static constexpr int SB = SB_FIT > 8 ? 8 : SB_FIT;
+  static constexpr uint32_t BAR_OFF = ACT_BYTES + SB * B_SLOT;
+  static constexpr uint32_t SMEM_BYTES = BAR_OFF + 512 + 1024;  // + barriers + alignment slack
+  static constexpr uint32_t TMEM_COLS = H;
+  static_assert(SB >= 2, "B ring too small");
+};
+
+__device__ __forceinline__ float sigmoid_fast(float v) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * v));
+  return fmaf(0.5f, t, 0.5f);
+}
+template <bool ACCURATE>
+__device__ __forceinline__ float sigmoid_(float v) {
+  if constexpr (ACCURATE) return 1.0f / (1.0f + __expf(-v));
+  else return sigmoid_fast(v);
+}
+
+// Store 32 consecutive values (cols c0..c0+31) of row `row` into a swizzled
+// K-major BF16 tile [H/64 blocks][128 rows][64]; lo = residual in SPLIT mode.
+template <int H, bool SPLIT>
+__device__ __forceinline__ void store_tile32(uint8_t* tile, uint32_t lo_off, int row, int c0, const float* v) {
+  uint8_t* blk = tile + (c0 >> 6) * (128 * 128);
+  const int q0 = (c0 & 63) >> 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float a = v[q * 8 + 2 * i], b = v[q * 8 + 2 * i + 1];
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+      hi[i] = *reinterpret_cast<uint32_t*>(&h2);
+      if constexpr (SPLIT) {
+        float ra = a - __bfloat162float(h2.x), rb = b - __bfloat162float(h2.y);
+        lo[i] = pack_bf16(ra, rb);
+      }
+    }
+    uint32_t off = sw128_off(row, q0 + q);
+    *reinterpret_cast<uint4*>(blk + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    if constexpr (SPLIT) *reinterpret_cast<uint4*>(blk + lo_off + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
+// 32 values -> global BF16 row segment (hi, and lo at +lo_off elements in SPLIT).
+template <bool SPLIT>
+__device__ __forceinline__ void store_bf32(__nv_bfloat16* p, long long lo_off, const float* v) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float a = v[q * 8 + 2 * i], b = v[q * 8 + 2 * i + 1];
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+      hi[i] = *reinterpret_cast<uint32_t*>(&h2);
+      if constexpr (SPLIT) lo[i] = pack_bf16(a - __bfloat162float(h2.x), b - __bfloat162float(h2.y));
+    }
+    reinterpret_cast<uint4*>(p)[q] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    if constexpr (SPLIT) reinterpret_cast<uint4*>(p + lo_off)[q] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+template <bool SPLIT>
+__device__ __forceinline__ void load_bf32(const __nv_bfloat16* p, long long lo_off, float* v) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u = reinterpret_cast<const uint4*>(p)[q];
+    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[q * 8 + i] = __bfloat162float(b[i]);
+    if constexpr (SPLIT) {
+      uint4 w = reinterpret_cast<const uint4*>(p + lo_off)[q];
+      const __nv_bfloat16* c = reinterpret_cast<const __nv_bfloat16*>(&w);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[q * 8 + i] += __bfloat162float(c[i]);
+    }
+  }
+}
+__device__ __forceinline__ void load_f32x32(const float* p, float* v) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float4 t = reinterpret_cast<const float4*>(p)[q];
+    v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+  }
+}
+__device__ __forceinline__ void store_f32x32(float* p, const float* v) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    reinterpret_cast<float4*>(p)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+}
+
+// Column sums of 32 values over the 32 lanes of a warp: afterwards lane l
+// holds the sum of column l (transpose-reduce, 31 shuffles, fixed order).
+__device__ __forceinline__ float warp_colsum32(float* v) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      bool up = (lane & w) != 0;
+      float send = up ? v[i] : v[i + w];
+      float keep = up ? v[i + w] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+    }
+  }
+  return v[0];
+}
+
+template <int H, bool SPLIT, bool BWD>
+__global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainParams p) {
+  using C = ChainCfg<H, SPLIT>;
+  constexpr int F = C::F;
+  constexpr int NB = C::NB;
+  constexpr int NH = H / NB;      // N-halves per step
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* act = smem;                       // ACT tile (and A ring)
+  uint8_t* bring = smem + C::ACT_BYTES;      // B ring
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* a_full = bars;                   // [SA]
+  uint64_t* a_empty = a_full + C::SA;        // [SA]
+  uint64_t* b_full = a_empty + C::SA;        // [SB]
+  uint64_t* b_empty = b_full + C::SB;        // [SB]
+  uint64_t* acc_full = b_empty + C::SB;      // MMA -> epilogue
+  uint64_t* acc_empty = acc_full + 1;        // epilogue -> MMA (TMEM drained)
+  uint64_t* act_full = acc_empty + 1;        // epilogue -> MMA (ACT written)
+  uint64_t* act_free = act_full + 1;         // MMA -> producer (no MMA reads ACT any more)
+  uint64_t* mma_idle = act_free + 1;         // MMA -> itself (all issued MMAs retired)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mma_idle + 1);
+
+  const int w = warp_id();
+  const int n_tiles = (p.M + 127) / 128;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::SA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < C::SB; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 128);
+    mbar_init(act_full, 128);
+    mbar_init(act_free, 1);
+    mbar_init(mma_idle, 1);
+    fence_barrier_init();
+  }
+  if (w == 0 && lane_id() == 0)
+    for (int i = 0; i < MAX_MAPS; ++i) tma_prefetch(&p.maps[i]);
+  if (w == 2) tmem_alloc(tslot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (w == 0) {
+    // ============================ TMA producer
+    if (elect_one()) {
+      int ai = 0, bi = 0, g = 0, naf = 0;  // A / B ring fills, global step, act_free phases
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int row0 = tile * 128;
+        for (int s = 0; s < p.n_steps; ++s, ++g) {
+          const Step& st = p.steps[s];
+          const bool tma_a = st.a_src == A_TMA;
+          if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) { mbar_wait(act_free, naf & 1); ++naf; }
+          for (int kc = 0; kc < st.K / 64; ++kc) {
+            if (tma_a) {
+              const int slot = ai % C::SA;
+              if (ai >= C::SA) mbar_wait(&a_empty[slot], ((ai / C::SA) - 1) & 1);
+              mbar_expect_tx(&a_full[slot], C::A_SLOT);
+              uint8_t* dstp = act + slot * C::A_SLOT;
+              const int k = kc * 64;
+              const int mi = (st.a_map1 >= 0 && k >= st.a_ksplit) ? st.a_map1 : st.a_map0;
+              const int kk = (st.a_map1 >= 0 && k >= st.a_ksplit) ? k - st.a_ksplit : k;
+              tma_load_2d(dstp, &p.maps[mi], &a_full[slot], kk, row0);
+              if constexpr (SPLIT) tma_load_2d(dstp + C::A_SLOT_HALF, &p.maps[mi + 1], &a_full[slot], kk, row0);
+              ++ai;
+            }
+            for (int nh = 0; nh < NH; ++nh) {
+              const int slot = bi % C::SB;
+              if (bi >= C::SB) mbar_wait(&b_empty[slot], ((bi / C::SB) - 1) & 1);
+              mbar_expect_tx(&b_full[slot], C::B_SLOT);
+              uint8_t* dstp = bring + slot * C::B_SLOT;
+              tma_load_2d(dstp, &p.maps[st.b_map], &b_full[slot], kc * 64, st.b_row0 + nh * NB);
+              if constexpr (SPLIT)
+                tma_load_2d(dstp + C::B_SLOT_HALF, &p.maps[st.b_map + 1], &b_full[slot], kc * 64, st.b_row0 + nh * NB);
+              ++bi;
+            }
+          }
+        }
+      }
+    }
+  } else if (w == 1) {
+    // ============================ MMA issuer
+    constexpr uint32_t idesc = idesc_bf16(NB, false, false);
+    int ai = 0, bi = 0, g = 0, nact = 0, nidle = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      for (int s = 0; s < p.n_steps; ++s, ++g) {
+        const Step& st = p.steps[s];
+        const bool tma_a = st.a_src == A_TMA;
+        if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) {
+          // let every issued MMA (the ones reading ACT) retire, then hand ACT
+          // to the producer as A-ring space; the pending epilogue overlaps.
+          if (elect_one()) mma_commit(mma_idle);
+          __syncwarp();
+          mbar_wait(mma_idle, nidle & 1);
+          ++nidle;
+          if (elect_one()) mbar_arrive(act_free);
+          __syncwarp();
+        }
+        if (g > 0) mbar_wait(acc_empty, (g - 1) & 1);
+        if (st.ctl & CTL_WAIT_ACT) { mbar_wait(act_full, nact & 1); ++nact; }
+        tc_fence_after();
+        for (int kc = 0; kc < st.K / 64; ++kc) {
+          int aslot = 0;
+          uint32_t a_base;
+          if (tma_a) {
+            aslot = ai % C::SA;
+            mbar_wait(&a_full[aslot], (ai / C::SA) & 1);
+            a_base = smem_u32(act + aslot * C::A_SLOT);
+          } else {
+            a_base = smem_u32(act + kc * (128 * 128));
+          }
+          const uint32_t a_lo = tma_a ? C::A_SLOT_HALF : C::ACT_HALF;
+          for (int nh = 0; nh < NH; ++nh) {
+            const int bslot = bi % C::SB;
+            mbar_wait(&b_full[bslot], (bi / C::SB) & 1);
+            tc_fence_after();
+            const uint32_t b_base = smem_u32(bring + bslot * C::B_SLOT);
+            if (elect_one()) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint32_t acc = (kc | k) != 0;
+                const uint32_t d = tmem + nh * NB;
+                uint64_t ad = sdesc_sw128(a_base + k * 32, 16, 1024);
+                uint64_t bd = sdesc_sw128(b_base + k * 32, 16, 1024);
+                mma_bf16(d, ad, bd, idesc, acc);
+                if constexpr (SPLIT) {
+                  uint64_t adl = sdesc_sw128(a_base + a_lo + k * 32, 16, 1024);
+                  uint64_t bdl = sdesc_sw128(b_base + C::B_SLOT_HALF + k * 32, 16, 1024);
+                  mma_bf16(d, adl, bd, idesc, 1);
+                  mma_bf16(d, ad, bdl, idesc, 1);
+                }
+              }
+              mma_commit(&b_empty[bslot]);
+            }
+            __syncwarp();
+            ++bi;
+          }
+          if (tma_a) {
+            if (elect_one()) mma_commit(&a_empty[aslot]);
+            __syncwarp();
+            ++ai;
+          }
+        }
+        if (elect_one()) mma_commit(acc_full);
+        __syncwarp();
+      }
+    }
+  } else if (w >= 4) {
+    // ============================ epilogue (thread = tile row = TMEM lane)
+    const int q = w & 3;
+    const int lane = lane_id();
+    const int trow = q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    float colacc[BWD ? NV_MAX : 1][BWD ? H / 32 : 1];
+    if constexpr (BWD) {
+#pragma unroll
+      for (int a = 0; a < NV_MAX; ++a)
+#pragma unroll
+        for (int b = 0; b < H / 32; ++b) colacc[a][b] = 0.f;
+    }
+    int g = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int r = tile * 128 + trow;
+      const bool valid = r < p.M;
+      const int rr = valid ? r : 0;
+      const int src = p.src ? p.src[rr] : 0;
+      const int dst = p.dst ? p.dst[rr] : 0;
+      for (int s = 0; s < p.n_steps; ++s, ++g) {
+        const Step& st = p.steps[s];
+        mbar_wait(acc_full, g & 1);
+        tc_fence_after();
+        bool wrote_act = false;
+        float v[32];
+        if (st.epi == EPI_SILU) {
+#pragma unroll 1
+          for (int c0 = 0; c0 < H; c0 += 32) {
+            tmem_ld32(tl + c0, v);
+            float g1[32], g2[32];
+            if (st.flags & EF_GATHER_P) {
+              load_f32x32(st.gather + (size_t)src * 2 * H + c0, g1);
+              load_f32x32(st.gather + (size_t)dst * 2 * H + H + c0, g2);
+            }
+            float sv[32], dv[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              float x = v[i] + __ldg(st.bias + c0 + i);
+              if (st.flags & EF_GATHER_P) x += g1[i] + g2[i];
+              float sg = sigmoid_<SPLIT>(x);
+              sv[i] = x * sg;
+              dv[i] = sg * (1.0f + x * (1.0f - sg));
+            }
+            store_tile32<H, SPLIT>(act, C::ACT_HALF, trow, c0, sv);
+            if (valid && (st.flags & EF_STORE_A)) store_bf32<SPLIT>(st.scr_a + (size_t)r * H + c0, st.lo_off, sv);
+            if (valid && (st.flags & EF_STORE_S)) store_bf32<SPLIT>(st.scr_s + (size_t)r * H + c0, st.lo_off, dv);
+          }
+          wrote_act = true;
+        } else if (st.epi == EPI_LN_FWD || st.epi == EPI_LN_BWD) {
+          // z = acc + b; two-pass mean / variance over the H columns of this row
+          float sum = 0.f;
+#pragma unroll 1
+          for (int c0 = 0; c0 < H; c0 += 32) {
+            tmem_ld32(tl + c0, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sum += v[i] + __ldg(st.bias + c0 + i);
+          }
+          const float mean = sum * (1.0f / H);
+          float sq = 0.f;
+#pragma unroll 1
+          for (int c0 = 0; c0 < H; c0 += 32) {
+            tmem_ld32(tl + c0, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) { float d = v[i] + __ldg(st.bias + c0 + i) - mean; sq += d * d; }
+          }
+          const float rstd = rsqrtf(sq * (1.0f / H) + p.eps);
+          if (st.epi == EPI_LN_FWD) {
+#pragma unroll 1
+            for (int c0 = 0; c0 < H; c0 += 32) {
+              tmem_ld32(tl + c0, v);
+              float res[32];
+              if (valid) load_f32x32(st.f_in + (size_t)r * st.ld_in + c0, res);
+              else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) res[i] = 0.f;
+              }
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                float xh = (v[i] + __ldg(st.bias + c0 + i) - mean) * rstd;
+                v[i] = res[i] + fmaf(__ldg(st.gamma + c0 + i), xh, __ldg(st.beta + c0 + i));
+              }
+              if (valid) {
+                store_f32x32(st.f_out + (size_t)r * st.ld_out + c0, v);
+                if (st.flags & EF_STORE_BF) store_bf32<SPLIT>(st.bf_out + (size_t)r * H + c0, st.bf_lo, v);
+              }
+              if (st.flags & EF_WRITE_ACT) store_tile32<H, SPLIT>(act, C::ACT_HALF, trow, c0, v);
+            }
+            wrote_act = (st.flags & EF_WRITE_ACT) != 0;
+          } else if constexpr (BWD) {
+            // LayerNorm backward: dx^ = dY*gamma; dz = rstd (dx^ - mean(dx^) - x^ mean(dx^ x^))
+            const bool has_g = valid && r < st.valid_in;
+            float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+            for (int cc = 0; cc < H / 32; ++cc) {
+              const int c0 = cc * 32;
+              tmem_ld32(tl + c0, v);
+              float dy[32], ga[32];
+              if (has_g) load_f32x32(st.f_in + (size_t)r * st.ld_in + c0, dy);
+              else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) dy[i] = 0.f;
+              }
+              if (valid && (st.flags & EF_GATHER_G)) {
+                load_f32x32(st.gather + (size_t)dst * H + c0, ga);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) dy[i] += ga[i];
+              }
+              float t1[32], t2[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                float xh = (v[i] + __ldg(st.bias + c0 + i) - mean) * rstd;
+                float dxh = dy[i] * __ldg(st.gamma + c0 + i);
+                s1 += dxh;
+                s2 += dxh * xh;
+                t1[i] = valid ? dy[i] * xh : 0.f;
+                t2[i] = valid ? dy[i] : 0.f;
+              }
+              colacc[0][cc] += warp_colsum32(t1);   // dgamma
+              colacc[1][cc] += warp_colsum32(t2);   // dbeta
+            }
+            s1 *= (1.0f / H);
+            s2 *= (1.0f / H);
+#pragma unroll
+            for (int cc = 0; cc < H / 32; ++cc) {
+              const int c0 = cc * 32;
+              tmem_ld32(tl + c0, v);
+              float dy[32], ga[32];
+              if (has_g) load_f32x32(st.f_in + (size_t)r * st.ld_in + c0, dy);
+              else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) dy[i] = 0.f;
+              }
+              if (valid && (st.flags & EF_GATHER_G)) {
+                load_f32x32(st.gather + (size_t)dst * H + c0, ga);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) dy[i] += ga[i];
+              }
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                float xh = (v[i] + __ldg(st.bias + c0 + i) - mean) * rstd;
+                float dxh = dy[i] * __ldg(st.gamma + c0 + i);
+                v[i] = valid ? rstd * (dxh - s1 - xh * s2) : 0.f;
+              }
+              store_tile32<H, SPLIT>(act, C::ACT_HALF, trow, c0, v);
+              if (valid) store_bf32<SPLIT>(st.scr_z + (size_t)r * H + c0, st.lo_off, v);
+              colacc[2][cc] += warp_colsum32(v);    // db_{m+1}
+            }
+            wrote_act = true;
+          }
+        } else if (st.epi == EPI_DSILU) {
+          if constexpr (BWD) {
+#pragma unroll
+            for (int cc = 0; cc < H / 32; ++cc) {
+              const int c0 = cc * 32;
+              tmem_ld32(tl + c0, v);
+              float sd[32];
+              if (valid) load_bf32<SPLIT>(st.scr_s + (size_t)r * H + c0, st.lo_off, sd);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = valid ? v[i] * sd[i] : 0.f;
+              store_tile32<H, SPLIT>(act, C::ACT_HALF, trow, c0, v);
+              if (valid) store_bf32<SPLIT>(st.scr_z + (size_t)r * H + c0, st.lo_off, v);
+              const float cs = warp_colsum32(v);
+              if (st.vec0 == 3) colacc[3][cc] += cs;  // db_m
+              else colacc[4][cc] += cs;               // db_{m-1}
+            }
+            wrote_act = true;
+          }
+        } else if (st.epi == EPI_STORE) {
+#pragma unroll 1
+          for (int c0 = 0; c0 < H; c0 += 32) {
+            tmem_ld32(tl + c0, v);
+            if (valid) store_f32x32(st.f_out + (size_t)r * st.ld_out + st.col0 + c0, v);
+          }
+        } else if (st.epi == EPI_ADD) {
+          const bool has_in = valid && r < st.valid_in;
+#pragma unroll 1
+          for (int c0 = 0; c0 < H; c0 += 32) {
+            tmem_ld32(tl + c0, v);
+            if (valid) {
+              float t[32];
+              if (has_in) {
+                load_f32x32(st.f_in + (size_t)r * st.ld_in + c0, t);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] += t[i];
+              }
+              if (st.flags & EF_GATHER_G) {
+                load_f32x32(st.gather + (size_t)dst * H + c0, t);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] += t[i];
+              }
+              store_f32x32(st.f_out + (size_t)r * st.ld_out + c0, v);
+            }
+          }
+        }
+        tc_fence_before();
+        if (wrote_act) fence_proxy_async_smem();
+        mbar_arrive(acc_empty);
+        if (wrote_act) mbar_arrive(act_full);
+      }
+    }
+    if constexpr (BWD) {
+      if (p.colsum) {
+        float* out = p.colsum + ((size_t)blockIdx.x * 4 + q) * NV_MAX * H;
+#pragma unroll
+        for (int a = 0; a < NV_MAX; ++a)
+#pragma unroll
+          for (int b = 0; b < H / 32; ++b) out[a * H + b * 32 + lane] = colacc[a][b];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 2) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+}  // namespace xmgn

@@ -1,0 +1,321 @@
+// Streaming / reduction kernels of the processor (see kernels.cuh) and the
+// split-K tcgen05 weight-gradient GEMM.  All reductions run in a fixed order:
+// no float atomics anywhere, so every result is bitwise run-to-run stable.
+#include <cuda_runtime.h>
+#include "kernels.cuh"
+#include "kernels_launch.h"
+
+namespace xmgn {
+
+// ---------------------------------------------------------------- weight packing
+__global__ void k_pack(const float* __restrict__ params, const PackJob* __restrict__ jobs, int njobs) {
+  for (int j = 0; j < njobs; ++j) {
+    const PackJob J = jobs[j];
+    const long long n = (long long)J.rows * J.cols;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+      const int r = (int)(t / J.cols), c = (int)(t % J.cols);
+      const float x = params[J.src + r * J.sr + c * J.sc];
+      const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+      J.dst[(long long)r * J.ld + c] = hi;
+      if (J.lo_off) J.dst[J.lo_off + (long long)r * J.ld + c] = __float2bfloat16_rn(x - __bfloat162float(hi));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- FP32 -> BF16 (hi [+ lo])
+__global__ void k_to_bf16(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, long long lo_off,
+                          long long n8) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n8; t += (long long)gridDim.x * blockDim.x) {
+    const float4 a = reinterpret_cast<const float4*>(in)[2 * t];
+    const float4 b = reinterpret_cast<const float4*>(in)[2 * t + 1];
+    float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+      hi[i] = *reinterpret_cast<uint32_t*>(&h);
+      lo[i] = pack_bf16(v[2 * i] - __bfloat162float(h.x), v[2 * i + 1] - __bfloat162float(h.y));
+    }
+    reinterpret_cast<uint4*>(out)[t] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    if (lo_off) reinterpret_cast<uint4*>(out + lo_off)[t] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
+// ---------------------------------------------------------------- aggregation (Eq. 2)
+// a_i = sum_{k in [off_i, off_{i+1})} e'_k, FP32 accumulation in CSR order, one
+// warp per destination, lanes over 16-byte channel slices; output BF16 hi[+lo]
+// (the node GEMM operand and the layer checkpoint).  HBM-bound.
+template <int H>
+__global__ void __launch_bounds__(256) k_aggregate(const int* __restrict__ off, const float* __restrict__ e,
+                                                   __nv_bfloat16* __restrict__ a, long long lo_off, int n) {
+  constexpr int V = H / 4 / 32;  // float4 per lane
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
+    float4 acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int k0 = off[i], k1 = off[i + 1];
+    for (int k = k0; k < k1; ++k) {
+      const float4* row = reinterpret_cast<const float4*>(e + (size_t)k * H);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        float4 x = __ldcs(row + lane + 32 * v);
+        acc[v].x += x.x; acc[v].y += x.y; acc[v].z += x.z; acc[v].w += x.w;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(acc[v].x, acc[v].y);
+      __nv_bfloat162 h1 = __floats2bfloat162_rn(acc[v].z, acc[v].w);
+      uint2 hv = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+      reinterpret_cast<uint2*>(a + (size_t)i * H)[lane + 32 * v] = hv;
+      if (lo_off) {
+        uint2 lv = make_uint2(pack_bf16(acc[v].x - __bfloat162float(h0.x), acc[v].y - __bfloat162float(h0.y)),
+                              pack_bf16(acc[v].z - __bfloat162float(h1.x), acc[v].w - __bfloat162float(h1.y)));
+        reinterpret_cast<uint2*>(a + lo_off + (size_t)i * H)[lane + 32 * v] = lv;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- segment sums of dZ1 (adjoint of the gathers)
+// D[i][0:H]  = sum_{k in seg(i), rev_k < e_act} dZ1[rev_k]   (out-edges of i: d/dP_src)
+// D[i][H:2H] = sum_{k in seg(i), k < e_act}     dZ1[k]       (in-edges of i:  d/dP_dst)
+// dZ1 rows live as BF16 hi[+lo]; sums in FP32 in CSR order; output BF16 hi[+lo].
+template <int H>
+__global__ void __launch_bounds__(256) k_segsum(const int* __restrict__ off, const int* __restrict__ rev,
+                                                const __nv_bfloat16* __restrict__ dz, long long dz_lo,
+                                                __nv_bfloat16* __restrict__ D, long long d_lo, int n, int e_act) {
+  constexpr int CH = 2 * H / 8;            // 16-byte chunks per output row
+  constexpr int V = CH / 32;
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
+    float acc[V][8];
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[v][t] = 0.f;
+    const int k0 = off[i], k1 = off[i + 1];
+    for (int k = k0; k < k1; ++k) {
+      const int rk = rev[k];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int ch = lane + 32 * v;
+        const bool srcpart = ch < H / 8;
+        const int kk = srcpart ? rk : k;
+        if (kk >= e_act) continue;
+        const int c8 = srcpart ? ch : ch - H / 8;
+        uint4 u = reinterpret_cast<const uint4*>(dz + (size_t)kk * H)[c8];
+        const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[v][t] += __bfloat162float(b[t]);
+        if (dz_lo) {
+          uint4 w = reinterpret_cast<const uint4*>(dz + dz_lo + (size_t)kk * H)[c8];
+          const __nv_bfloat16* c = reinterpret_cast<const __nv_bfloat16*>(&w);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) acc[v][t] += __bfloat162float(c[t]);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int ch = lane + 32 * v;
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(acc[v][2 * t], acc[v][2 * t + 1]);
+        hi[t] = *reinterpret_cast<uint32_t*>(&h);
+        lo[t] = pack_bf16(acc[v][2 * t] - __bfloat162float(h.x), acc[v][2 * t + 1] - __bfloat162float(h.y));
+      }
+      reinterpret_cast<uint4*>(D + (size_t)i * 2 * H)[ch] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      if (d_lo) reinterpret_cast<uint4*>(D + d_lo + (size_t)i * 2 * H)[ch] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- weight gradient dW = A^T dZ (split-K)
+// D[m = input feature][n = output feature] += sum_rows A[row][m] dZ[row][n].
+// Both operands are read straight from their row-major BF16 tensors as
+// MN-major UMMA tiles (TMA boxes of 64 features x 64 rows), so no transposed
+// copies exist.  gridDim = (Hin/128, Hout/NT, n_split); each CTA reduces a
+// fixed row range and writes its FP32 partial; k_reduce_part sums the splits
+// in order.
+template <int NT, bool SPLIT>
+__global__ void __launch_bounds__(128, 1) k_wgrad(const __grid_constant__ WgradParams p) {
+  constexpr int F = SPLIT ? 2 : 1;
+  constexpr uint32_t A_HALF = 128 * 64 * 2, B_HALF = NT * 64 * 2;
+  constexpr uint32_t STAGE = F * (A_HALF + B_HALF);
+  constexpr int S = (int)((220u * 1024u) / STAGE) > 6 ? 6 : (int)((220u * 1024u) / STAGE);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE);
+  uint64_t* empty = full + S;
+  uint64_t* done = empty + S;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  const int w = warp_id();
+  const int mt = blockIdx.x, nt = blockIdx.y, sp = blockIdx.z;
+  const CUtensorMap* am = mt < p.a_split_tiles ? &p.a0 : &p.a1;
+  const CUtensorMap* aml = mt < p.a_split_tiles ? &p.a0lo : &p.a1lo;
+  const int acol = (mt < p.a_split_tiles ? mt : mt - p.a_split_tiles) * 128;
+  const int bcol = p.b_col0 + nt * NT;
+  const int chunks = (p.rows + 63) / 64;
+  const int c0 = (int)((long long)chunks * sp / p.n_split), c1 = (int)((long long)chunks * (sp + 1) / p.n_split);
+  const int nk = c1 - c0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (w == 2) tmem_alloc(tslot, NT);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (w == 0) {
+    if (elect_one()) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % S;
+        if (kb >= S) mbar_wait(&empty[s], ((kb / S) - 1) & 1);
+        mbar_expect_tx(&full[s], STAGE);
+        uint8_t* st = smem + s * STAGE;
+        const int row = (c0 + kb) * 64;
+        tma_load_2d(st, am, &full[s], acol, row);
+        tma_load_2d(st + 8192, am, &full[s], acol + 64, row);
+        for (int j = 0; j < NT / 64; ++j) tma_load_2d(st + A_HALF + j * 8192, &p.b, &full[s], bcol + j * 64, row);
+        if constexpr (SPLIT) {
+          uint8_t* sl = st + A_HALF + B_HALF;
+          tma_load_2d(sl, aml, &full[s], acol, row);
+          tma_load_2d(sl + 8192, aml, &full[s], acol + 64, row);
+          for (int j = 0; j < NT / 64; ++j) tma_load_2d(sl + A_HALF + j * 8192, &p.blo, &full[s], bcol + j * 64, row);
+        }
+      }
+    }
+  } else if (w == 1) {
+    constexpr uint32_t idesc = idesc_bf16(NT, true, true);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % S;
+      mbar_wait(&full[s], (kb / S) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t a0 = smem_u32(smem + s * STAGE), b0 = a0 + A_HALF;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint64_t ad = sdesc_sw128(a0 + k * 2048, 8192, 1024);
+          uint64_t bd = sdesc_sw128(b0 + k * 2048, 8192, 1024);
+          mma_bf16(tmem, ad, bd, idesc, (kb | k) != 0);
+          if constexpr (SPLIT) {
+            const uint32_t a0l = a0 + A_HALF + B_HALF, b0l = a0l + A_HALF;
+            mma_bf16(tmem, sdesc_sw128(a0l + k * 2048, 8192, 1024), bd, idesc, 1);
+            mma_bf16(tmem, ad, sdesc_sw128(b0l + k * 2048, 8192, 1024), idesc, 1);
+          }
+        }
+        mma_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+    if (elect_one()) mma_commit(done);
+    __syncwarp();
+  }
+  __syncwarp();
+  const int m = mt * 128 + w * 32 + lane_id();
+  float* out = p.part + ((size_t)sp * p.Hin + m) * p.Hout + nt * NT;
+  if (nk > 0) {
+    mbar_wait(done, 0);
+    tc_fence_after();
+    for (int c = 0; c < NT; c += 32) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(w * 32) << 16) + c, v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(out + c)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+  } else {
+    for (int c = 0; c < NT; ++c) out[c] = 0.f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 2) tmem_dealloc(tmem, NT);
+}
+
+// grad[i] += sum_{s < S} part[s][i]  (fixed order)
+__global__ void k_reduce_part(const float* __restrict__ part, int S, long long n, float* __restrict__ grad) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < S; ++k) s += part[k * n + i];
+    grad[i] += s;
+  }
+}
+
+// Column-sum partials [nblk][4][NV][H] -> grad[dst[v] + c] += sum (fixed order).
+__global__ void k_reduce_colsum(const float* __restrict__ part, int nblk, int nv, int H, ColsumDst dsts,
+                                float* __restrict__ grad) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nv * H) return;
+  const int v = t / H, c = t % H;
+  if (dsts.off[v] < 0) return;
+  float s = 0.f;
+  for (int b = 0; b < nblk * 4; ++b) s += part[((size_t)b * NV_COLSUM + v) * H + c];
+  grad[dsts.off[v] + c] += s;
+}
+
+__global__ void k_nonfinite(const float* __restrict__ x, long long n, int* __restrict__ flag) {
+  int bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
+// ---------------------------------------------------------------- launchers
+void launch_pack(const float* params, const PackJob* jobs, int njobs, cudaStream_t st) {
+  k_pack<<<592, 256, 0, st>>>(params, jobs, njobs);
+}
+void launch_to_bf16(const float* in, __nv_bfloat16* out, long long lo_off, long long n, cudaStream_t st) {
+  if (n <= 0) return;
+  long long n8 = n / 8;
+  int blocks = (int)std::min<long long>((n8 + 255) / 256, 148 * 16);
+  k_to_bf16<<<blocks, 256, 0, st>>>(in, out, lo_off, n8);
+}
+void launch_aggregate(int H, const int* off, const float* e, __nv_bfloat16* a, long long lo_off, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  int blocks = std::min((n + 7) / 8, 148 * 16);
+  if (H == 128) k_aggregate<128><<<blocks, 256, 0, st>>>(off, e, a, lo_off, n);
+  else if (H == 256) k_aggregate<256><<<blocks, 256, 0, st>>>(off, e, a, lo_off, n);
+  else k_aggregate<512><<<blocks, 256, 0, st>>>(off, e, a, lo_off, n);
+}
+void launch_segsum(int H, const int* off, const int* rev, const __nv_bfloat16* dz, long long dz_lo, __nv_bfloat16* D,
+                   long long d_lo, int n, int e_act, cudaStream_t st) {
+  if (n <= 0) return;
+  int blocks = std::min((n + 7) / 8, 148 * 16);
+  if (H == 128) k_segsum<128><<<blocks, 256, 0, st>>>(off, rev, dz, dz_lo, D, d_lo, n, e_act);
+  else if (H == 256) k_segsum<256><<<blocks, 256, 0, st>>>(off, rev, dz, dz_lo, D, d_lo, n, e_act);
+  else k_segsum<512><<<blocks, 256, 0, st>>>(off, rev, dz, dz_lo, D, d_lo, n, e_act);
+}
+
+template <int NT, bool SPLIT>
+static void wgrad_launch(const WgradParams& p, dim3 grid, cudaStream_t st) {
+  constexpr int F = SPLIT ? 2 : 1;
+  constexpr uint32_t STAGE = F * (128 * 64 * 2 + NT * 64 * 2);
+  constexpr int S = (int)((220u * 1024u) / STAGE) > 6 ? 6 : (int)((220u * 1024u) / STAGE);
+  size_t smem = 1024 + S * STAGE + 256;
+  auto kern = k_wgrad<NT, SPLIT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, 128, smem, st>>>(p);
+}
+void launch_wgrad(const WgradParams& p, bool split, cudaStream_t st) {
+  const int NT = p.Hout >= 256 ? 256 : p.Hout;
+  dim3 grid(p.Hin / 128, p.Hout / NT, p.n_split);
+  if (NT == 256) { if (split) wgrad_launch<256, true>(p, grid, st); else wgrad_launch<256, false>(p, grid, st); }
+  else { if (split) wgrad_launch<128, true>(p, grid, st); else wgrad_launch<128, false>(p, grid, st); }
+}
+void launch_reduce_part(const float* part, int S, long long n, float* grad, cudaStream_t st) {
+  int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+  k_reduce_part<<<blocks, 256, 0, st>>>(part, S, n, grad);
+}
+void launch_reduce_colsum(const float* part, int nblk, int nv, int H, ColsumDst d, float* grad, cudaStream_t st) {
+  k_reduce_colsum<<<(nv * H + 255) / 256, 256, 0, st>>>(part, nblk, nv, H, d, grad);
+}
+void launch_nonfinite(const float* x, long long n, int* flag, cudaStream_t st) {
+  k_nonfinite<<<592, 256, 0, st>>>(x, n, flag);
+}
+
+}  // namespace xmgn

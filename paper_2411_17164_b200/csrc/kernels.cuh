@@ -1,0 +1,28 @@
+// Streaming kernels around the GEMM chains: weight packing, BF16 staging,
+// the deterministic segmented sums (aggregation, its adjoint), split-K weight
+// gradients on tcgen05 and fixed-order reductions.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda.h>
+#include "tc.cuh"
+
+namespace xmgn {
+
+struct PackJob {            // out[r][c] = bf16(params[src + r*sr + c*sc]), r < rows, c < cols
+  __nv_bfloat16* dst;
+  long long lo_off;         // lo copy at dst + lo_off (0 = none)
+  int ld, rows, cols;
+  long long src, sr, sc;
+};
+
+struct WgradParams {
+  CUtensorMap a0, a0lo, a1, a1lo, b, blo;  // MN-major operands (row-major BF16 activations)
+  int a_split_tiles;    // M tiles [0, a_split_tiles) come from a0, the rest from a1
+  int b_col0;           // first B column (feature) of this weight
+  int rows;             // reduction length (rows of the activation tensors)
+  int n_split;          // split-K factor (gridDim.z)
+  int Hin, Hout;        // dW is [Hin][Hout]
+  float* part;          // [n_split][Hin][Hout]
+};
+
+}  // namespace xmgn

@@ -1,0 +1,613 @@
+// Workspace, forward and backward of the processor on one GPU (call
+// stacks 3-4).  Host code only sequences launches; every arithmetic step runs in
+// the kernels of chain.cuh / kernels.cu.
+//
+// Algorithmic restatement used here (identical function to include/xmgn.h):
+//   [e | h_src | h_dst] W1e = e W1e_e + (h W1e_s)[src] + (h W1e_d)[dst],
+// so each layer first projects the nodes, P = h [W1e_s | W1e_d] (N x 2H, FP32),
+// and the edge MLP's first GEMM has K = H instead of 3H.
+// The backward mirrors it: d(P_src)[i] / d(P_dst)[i] are segment sums of dZ1
+// over out-/in-edges (rev permutation; no atomics), then one node-level GEMM.
+//
+// Halo shrinking: with ring-major numbering layer l only
+// updates destinations of ring <= L-l, a prefix of nodes (n_l) and of edges
+// (E_l); the skipped rows feed only discarded halo outputs.
+#include <cuda_runtime.h>
+#include <cstring>
+#include <vector>
+#include "graph.h"
+#include "kernels_launch.h"
+#include "tmap.h"
+
+namespace xmgn {
+
+typedef __nv_bfloat16 bf16;
+
+struct DPart {
+  int *off = nullptr, *src = nullptr, *dst = nullptr, *rev = nullptr;
+};
+
+struct BfBuf {       // BF16 tensor with an optional lo half (FP32 check mode)
+  bf16* p = nullptr;
+  long long lo = 0;  // element offset of the lo half (0 when not split)
+};
+
+}  // namespace xmgn
+
+struct xmgn_workspace {
+  const xmgn_graph* g = nullptr;
+  xmgn_model_cfg cfg{};
+  int dev = 0, H = 0, L = 0, m = 0, sms = 148;
+  bool split = false;
+  int64_t Nmax = 0, Emax = 0, Rmax = 0;
+  std::vector<xmgn::DPart> dparts;
+  std::vector<void*> allocs;
+  size_t bytes = 0;
+  // packed weights
+  int S1 = 0, S2 = 0;
+  xmgn::BfBuf wk1, wk2;
+  xmgn::PackJob* d_jobs = nullptr;
+  int njobs = 0;
+  // checkpoints (per layer) and live streams
+  xmgn::BfBuf e_ck, h_ck, a_ck;   // [L][Emax|Nmax][H]
+  float *e_buf[2] = {nullptr, nullptr}, *h_buf[2] = {nullptr, nullptr}, *P = nullptr;
+  // backward
+  float *Ge = nullptr, *Gh = nullptr, *Ga = nullptr;
+  xmgn::BfBuf scrA[2], scrS[2], scrZ[3], D;
+  float* part = nullptr;  // wgrad split-K partials
+  int part_splits = 0;
+  float* colsum = nullptr;
+  int* d_flag = nullptr;
+  int last_fwd = -1;
+};
+
+namespace xmgn {
+
+static void* dalloc(xmgn_workspace* ws, size_t bytes) {
+  void* p = nullptr;
+  bytes = (bytes + 255) & ~size_t(255);
+  XMGN_CUDA(cudaMalloc(&p, bytes ? bytes : 256), "xmgn_workspace_create: cudaMalloc");
+  ws->allocs.push_back(p);
+  ws->bytes += bytes;
+  return p;
+}
+static BfBuf bfalloc(xmgn_workspace* ws, size_t count) {
+  BfBuf b;
+  const int F = ws->split ? 2 : 1;
+  b.p = static_cast<bf16*>(dalloc(ws, count * F * sizeof(bf16)));
+  b.lo = ws->split ? (long long)count : 0;
+  return b;
+}
+
+// ---- parameter layout (include/xmgn.h; an independent restatement of SURVEY §8(b))
+struct Layout {
+  int H, L, m;
+  int64_t bs(int kin) const { return (int64_t)kin * H + H + (int64_t)m * ((int64_t)H * H + H) + 2 * (int64_t)H; }
+  int64_t per() const { return bs(3 * H) + bs(2 * H); }
+  int64_t base(int l, int blk) const { return l * per() + (blk ? bs(3 * H) : 0); }
+  int kin(int blk) const { return blk ? 2 * H : 3 * H; }
+  int64_t W(int l, int blk, int j) const {
+    return base(l, blk) + (j == 0 ? 0 : (int64_t)kin(blk) * H + H + (int64_t)(j - 1) * ((int64_t)H * H + H));
+  }
+  int64_t b(int l, int blk, int j) const { return W(l, blk, j) + (int64_t)(j == 0 ? kin(blk) : H) * H; }
+  int64_t gamma(int l, int blk) const { return base(l, blk) + (int64_t)kin(blk) * H + H + (int64_t)m * ((int64_t)H * H + H); }
+  int64_t beta(int l, int blk) const { return gamma(l, blk) + H; }
+  int64_t count() const { return (int64_t)L * per(); }
+};
+
+// Wk1 slots (rows of H, K = H): forward W^T and dgrad W for every H-wide operand.
+enum { SL_E1T = 0, SL_PST = 1, SL_PDT = 2, SL_EJT = 3 };
+static int sl_njt(int m) { return 3 + m; }        // node W_j^T, j = 1..m
+static int sl_ej(int m) { return 3 + 2 * m; }     // edge W_j (dgrad), j = 1..m
+static int sl_e1e(int m) { return 3 + 3 * m; }    // edge W_0 rows of e (dgrad)
+static int sl_nj(int m) { return 4 + 3 * m; }     // node W_j (dgrad), j = 1..m
+static int sl_n1h(int m) { return 4 + 4 * m; }    // node W_0 rows of h (dgrad)
+static int sl_n1a(int m) { return 5 + 4 * m; }    // node W_0 rows of agg (dgrad)
+static int n_sl1(int m) { return 6 + 4 * m; }
+enum { SL2_N1T = 0, SL2_SD = 1 };                 // Wk2 (K = 2H): node W_0^T; [W_s | W_d] (proj bwd)
+
+static std::vector<PackJob> pack_jobs(xmgn_workspace* ws) {
+  const int H = ws->H, m = ws->m;
+  Layout Ly{H, ws->L, m};
+  std::vector<PackJob> J;
+  auto job = [&](BfBuf& buf, int ld, long long row0, int col0, int rows, int cols, long long src, long long sr,
+                 long long sc) {
+    PackJob j;
+    j.dst = buf.p + row0 * ld + col0;
+    j.lo_off = buf.lo;
+    j.ld = ld; j.rows = rows; j.cols = cols; j.src = src; j.sr = sr; j.sc = sc;
+    J.push_back(j);
+  };
+  for (int l = 0; l < ws->L; ++l) {
+    auto r1 = [&](int slot) { return (long long)(l * ws->S1 + slot) * H; };
+    auto r2 = [&](int slot) { return (long long)(l * ws->S2 + slot) * H; };
+    const int64_t We0 = Ly.W(l, 0, 0), Wn0 = Ly.W(l, 1, 0);
+    // transposed (forward, B[n=out][k=in] = W[in][out])
+    job(ws->wk1, H, r1(SL_E1T), 0, H, H, We0, 1, H);
+    job(ws->wk1, H, r1(SL_PST), 0, H, H, We0 + (int64_t)H * H, 1, H);
+    job(ws->wk1, H, r1(SL_PDT), 0, H, H, We0 + 2 * (int64_t)H * H, 1, H);
+    for (int j = 1; j <= m; ++j) {
+      job(ws->wk1, H, r1(SL_EJT + j - 1), 0, H, H, Ly.W(l, 0, j), 1, H);
+      job(ws->wk1, H, r1(sl_njt(m) + j - 1), 0, H, H, Ly.W(l, 1, j), 1, H);
+      // as stored (dgrad, B[n=in][k=out] = W[in][out])
+      job(ws->wk1, H, r1(sl_ej(m) + j - 1), 0, H, H, Ly.W(l, 0, j), H, 1);
+      job(ws->wk1, H, r1(sl_nj(m) + j - 1), 0, H, H, Ly.W(l, 1, j), H, 1);
+    }
+    job(ws->wk1, H, r1(sl_e1e(m)), 0, H, H, We0, H, 1);
+    job(ws->wk1, H, r1(sl_n1h(m)), 0, H, H, Wn0, H, 1);
+    job(ws->wk1, H, r1(sl_n1a(m)), 0, H, H, Wn0 + (int64_t)H * H, H, 1);
+    job(ws->wk2, 2 * H, r2(SL2_N1T), 0, H, 2 * H, Wn0, 1, H);
+    job(ws->wk2, 2 * H, r2(SL2_SD), 0, H, H, We0 + (int64_t)H * H, H, 1);
+    job(ws->wk2, 2 * H, r2(SL2_SD), H, H, H, We0 + 2 * (int64_t)H * H, H, 1);
+  }
+  return J;
+}
+
+// ---- tensor maps
+static CUtensorMap map_rows(const bf16* base, long long rows, int width, int box_rows) {
+  return tmap_bf16(base, (uint64_t)width, (uint64_t)(rows > 0 ? rows : 1), (uint64_t)width, 64, box_rows);
+}
+
+// ---- chain program builder
+struct Prog {
+  ChainParams p;
+  int n = 0;
+  Prog() { std::memset(&p, 0, sizeof(p)); }
+  Step& add() {
+    Step& s = p.steps[n++];
+    std::memset(&s, 0, sizeof(s));
+    s.a_map1 = -1;
+    return s;
+  }
+};
+
+static bool epi_writes_act(const Step& s) {
+  switch (s.epi) {
+    case EPI_SILU: case EPI_LN_BWD: case EPI_DSILU: return true;
+    case EPI_LN_FWD: return (s.flags & EF_WRITE_ACT) != 0;
+    default: return false;
+  }
+}
+
+// Derive the ACT hand-off controls (chain.cuh) and launch.
+static void run_prog(xmgn_workspace* ws, Prog& pr, int M, const int* src, const int* dst, bool bwd, cudaStream_t st) {
+  if (M <= 0) return;
+  ChainParams& p = pr.p;
+  p.n_steps = pr.n;
+  p.M = M;
+  p.src = src;
+  p.dst = dst;
+  p.eps = ws->cfg.ln_eps;
+  const int n = pr.n;
+  if (epi_writes_act(p.steps[n - 1])) throw Fail{set_error(XMGN_ESTATE, "internal: program ends writing ACT")};
+  for (int s = 0; s < n; ++s) {
+    Step& S = p.steps[s];
+    S.ctl = 0;
+    if (S.a_src == A_ACT) {
+      if (s == 0) throw Fail{set_error(XMGN_ESTATE, "internal: program starts with A_ACT")};
+      if (epi_writes_act(p.steps[s - 1])) S.ctl |= CTL_WAIT_ACT;
+    } else {
+      // ACT used since the previous A_TMA step (cyclically)?
+      bool used = false;
+      for (int t = 1; t < n; ++t) {
+        const Step& T = p.steps[(s - t + n) % n];
+        if (T.a_src == A_ACT || epi_writes_act(T)) used = true;
+        if (T.a_src == A_TMA) break;
+      }
+      if (used) S.ctl |= CTL_NEED_ACT_FREE;
+    }
+  }
+  // weight maps
+  const int NB = ws->H < 256 ? ws->H : 256;
+  const long long r1 = (long long)ws->L * ws->S1 * ws->H, r2 = (long long)ws->L * ws->S2 * ws->H;
+  p.maps[0] = tmap_bf16(ws->wk1.p, ws->H, r1, ws->H, 64, NB);
+  p.maps[1] = ws->split ? tmap_bf16(ws->wk1.p + ws->wk1.lo, ws->H, r1, ws->H, 64, NB) : p.maps[0];
+  p.maps[2] = tmap_bf16(ws->wk2.p, 2 * ws->H, r2, 2 * ws->H, 64, NB);
+  p.maps[3] = ws->split ? tmap_bf16(ws->wk2.p + ws->wk2.lo, 2 * ws->H, r2, 2 * ws->H, 64, NB) : p.maps[2];
+  const int tiles = (M + 127) / 128;
+  const int grid = tiles < ws->sms ? tiles : ws->sms;
+  p.colsum = bwd ? ws->colsum : nullptr;
+  launch_chain(ws->H, ws->split, bwd, p, grid, st);
+  XMGN_CUDA(cudaGetLastError(), "chain kernel launch");
+}
+
+static void set_a(xmgn_workspace* ws, Prog& pr, int slot, const BfBuf& b, long long rows, int width) {
+  pr.p.maps[slot] = map_rows(b.p, rows, width, 128);
+  pr.p.maps[slot + 1] = ws->split ? map_rows(b.p + b.lo, rows, width, 128) : pr.p.maps[slot];
+}
+
+static BfBuf at(const BfBuf& b, long long elem) { return BfBuf{b.p + elem, b.lo}; }
+
+// weight-gradient GEMM + fixed-order reduction into grad[dst .. dst + Hin*Hout)
+static void wgrad(xmgn_workspace* ws, const BfBuf& a0, const BfBuf& a1, int a_width, int a_split_tiles, const BfBuf& b,
+                  int b_width, int b_col0, long long rows, int Hin, float* grad, long long dst, cudaStream_t st) {
+  if (rows <= 0) return;
+  const int H = ws->H;
+  WgradParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.a0 = tmap_bf16(a0.p, a_width, rows, a_width, 64, 64);
+  p.a0lo = ws->split ? tmap_bf16(a0.p + a0.lo, a_width, rows, a_width, 64, 64) : p.a0;
+  const BfBuf& a1r = a1.p ? a1 : a0;
+  p.a1 = tmap_bf16(a1r.p, a_width, rows, a_width, 64, 64);
+  p.a1lo = ws->split ? tmap_bf16(a1r.p + a1r.lo, a_width, rows, a_width, 64, 64) : p.a1;
+  p.b = tmap_bf16(b.p, b_width, rows, b_width, 64, 64);
+  p.blo = ws->split ? tmap_bf16(b.p + b.lo, b_width, rows, b_width, 64, 64) : p.b;
+  p.a_split_tiles = a_split_tiles;
+  p.b_col0 = b_col0;
+  p.rows = (int)rows;
+  p.Hin = Hin;
+  p.Hout = H;
+  const int NT = H >= 256 ? 256 : H;
+  const int tiles = (Hin / 128) * (H / NT);
+  const int chunks = (int)((rows + 63) / 64);
+  int S = (2 * ws->sms + tiles - 1) / tiles;
+  if (S > chunks) S = chunks;
+  if (S > ws->part_splits) S = ws->part_splits;
+  if (S < 1) S = 1;
+  p.n_split = S;
+  p.part = ws->part;
+  launch_wgrad(p, ws->split, st);
+  XMGN_CUDA(cudaGetLastError(), "wgrad launch");
+  launch_reduce_part(ws->part, S, (long long)Hin * H, grad + dst, st);
+}
+
+static void colsum_reduce(xmgn_workspace* ws, int blk, int l, float* grad, int grid_used, cudaStream_t st) {
+  Layout Ly{ws->H, ws->L, ws->m};
+  ColsumDst d;
+  for (int v = 0; v < NV_MAX; ++v) d.off[v] = -1;
+  d.off[0] = Ly.gamma(l, blk);
+  d.off[1] = Ly.beta(l, blk);
+  d.off[2] = Ly.b(l, blk, ws->m);
+  d.off[3] = Ly.b(l, blk, ws->m - 1);
+  if (ws->m >= 2) d.off[4] = Ly.b(l, blk, ws->m - 2);
+  launch_reduce_colsum(ws->colsum, grid_used, NV_MAX, ws->H, d, grad, st);
+}
+
+}  // namespace xmgn
+
+using namespace xmgn;
+
+extern "C" size_t xmgn_param_count(const xmgn_model_cfg* c) {
+  if (!c || c->hidden <= 0 || c->layers <= 0 || c->mlp_hidden_layers < 1) return 0;
+  Layout Ly{c->hidden, c->layers, c->mlp_hidden_layers};
+  return (size_t)Ly.count();
+}
+
+extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_model_cfg* cfg, xmgn_workspace** out) {
+  return guarded("xmgn_workspace_create", [&]() -> xmgn_status {
+    if (!g || !cfg || !out) return set_error(XMGN_EINVAL, "xmgn_workspace_create: null argument");
+    *out = nullptr;
+    const int H = cfg->hidden, L = cfg->layers, m = cfg->mlp_hidden_layers;
+    if (!(H == 128 || H == 256 || H == 512))
+      return set_error(XMGN_EUNSUPPORTED, "xmgn_workspace_create: hidden=%d (kernels built for 128, 256, 512)", H);
+    if (m < 1 || m > 2) return set_error(XMGN_EUNSUPPORTED, "xmgn_workspace_create: mlp_hidden_layers=%d (1 or 2)", m);
+    if (L < 1) return set_error(XMGN_EINVAL, "xmgn_workspace_create: layers=%d", L);
+    if (cfg->precision == XMGN_PREC_FP32_CHECK && H != 128)
+      return set_error(XMGN_EUNSUPPORTED, "xmgn_workspace_create: FP32 check mode is built for hidden=128 only");
+    if (cfg->precision != XMGN_PREC_BF16 && cfg->precision != XMGN_PREC_FP32_CHECK)
+      return set_error(XMGN_EINVAL, "xmgn_workspace_create: precision=%d", cfg->precision);
+    if (L > g->depth)
+      return set_error(XMGN_EHALO,
+                       "xmgn_workspace_create: layers=%d exceeds halo_depth=%d (owned outputs would differ from the "
+                       "full graph, PAPER.md:172)",
+                       L, g->depth);
+    XMGN_CUDA(cudaSetDevice(g->device), "xmgn_workspace_create: cudaSetDevice");
+    auto* ws = new xmgn_workspace();
+    try {
+      ws->g = g;
+      ws->cfg = *cfg;
+      ws->dev = g->device;
+      ws->H = H; ws->L = L; ws->m = m;
+      ws->split = cfg->precision == XMGN_PREC_FP32_CHECK;
+      cudaDeviceGetAttribute(&ws->sms, cudaDevAttrMultiProcessorCount, g->device);
+      for (const Part& P : g->parts) {
+        ws->Nmax = std::max(ws->Nmax, P.n_local);
+        ws->Emax = std::max(ws->Emax, P.e_local);
+      }
+      ws->Rmax = std::max(ws->Nmax, ws->Emax);
+      // graph arrays
+      for (const Part& P : g->parts) {
+        DPart d;
+        std::vector<int32_t> off32(P.offsets.begin(), P.offsets.end());
+        d.off = (int*)dalloc(ws, off32.size() * 4);
+        d.src = (int*)dalloc(ws, P.e_local * 4);
+        d.dst = (int*)dalloc(ws, P.e_local * 4);
+        d.rev = (int*)dalloc(ws, P.e_local * 4);
+        XMGN_CUDA(cudaMemcpy(d.off, off32.data(), off32.size() * 4, cudaMemcpyHostToDevice), "upload");
+        XMGN_CUDA(cudaMemcpy(d.src, P.src.data(), P.e_local * 4, cudaMemcpyHostToDevice), "upload");
+        XMGN_CUDA(cudaMemcpy(d.dst, P.dst.data(), P.e_local * 4, cudaMemcpyHostToDevice), "upload");
+        XMGN_CUDA(cudaMemcpy(d.rev, P.rev.data(), P.e_local * 4, cudaMemcpyHostToDevice), "upload");
+        ws->dparts.push_back(d);
+      }
+      const size_t NH = (size_t)ws->Nmax * H, EH = (size_t)ws->Emax * H, RH = (size_t)ws->Rmax * H;
+      ws->S1 = n_sl1(m);
+      ws->S2 = 2;
+      ws->wk1 = bfalloc(ws, (size_t)L * ws->S1 * H * H);
+      ws->wk2 = bfalloc(ws, (size_t)L * ws->S2 * H * 2 * H);
+      std::vector<PackJob> jobs = pack_jobs(ws);
+      ws->njobs = (int)jobs.size();
+      ws->d_jobs = (PackJob*)dalloc(ws, jobs.size() * sizeof(PackJob));
+      XMGN_CUDA(cudaMemcpy(ws->d_jobs, jobs.data(), jobs.size() * sizeof(PackJob), cudaMemcpyHostToDevice), "upload");
+      ws->e_ck = bfalloc(ws, (size_t)L * EH);
+      ws->h_ck = bfalloc(ws, (size_t)L * NH);
+      ws->a_ck = bfalloc(ws, (size_t)L * NH);
+      for (int i = 0; i < 2; ++i) {
+        ws->e_buf[i] = (float*)dalloc(ws, EH * 4);
+        ws->h_buf[i] = (float*)dalloc(ws, NH * 4);
+      }
+      ws->P = (float*)dalloc(ws, 2 * NH * 4);
+      ws->Ge = (float*)dalloc(ws, EH * 4);
+      ws->Gh = (float*)dalloc(ws, NH * 4);
+      ws->Ga = (float*)dalloc(ws, NH * 4);
+      for (int j = 0; j < m; ++j) { ws->scrA[j] = bfalloc(ws, RH); ws->scrS[j] = bfalloc(ws, RH); }
+      for (int j = 0; j <= m; ++j) ws->scrZ[j] = bfalloc(ws, RH);
+      ws->D = bfalloc(ws, 2 * NH);
+      ws->part_splits = 64;
+      ws->part = (float*)dalloc(ws, (size_t)ws->part_splits * 2 * H * H * 4);
+      ws->colsum = (float*)dalloc(ws, (size_t)ws->sms * 4 * NV_MAX * H * 4);
+      ws->d_flag = (int*)dalloc(ws, 4);
+    } catch (...) {
+      xmgn_workspace_free(ws);
+      throw;
+    }
+    *out = ws;
+    return XMGN_OK;
+  });
+}
+
+extern "C" size_t xmgn_workspace_bytes(const xmgn_workspace* ws) { return ws ? ws->bytes : 0; }
+
+extern "C" void xmgn_workspace_free(xmgn_workspace* ws) {
+  if (!ws) return;
+  for (void* p : ws->allocs) cudaFree(p);
+  delete ws;
+}
+
+static inline int64_t n_at(const Part& P, int L, int l) {  // rows of layer l (ring <= L-l)
+  return P.ring_nodes[L - l + 1];
+}
+static inline int64_t e_at(const Part& P, int L, int l) { return P.ring_edges[L - l + 1]; }
+
+extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const float* params, const float* h0,
+                                          const float* e0, float* h_out, void* stream) {
+  return guarded("xmgn_processor_fwd", [&]() -> xmgn_status {
+    if (!ws || !params || !h0 || !e0 || !h_out) return set_error(XMGN_EINVAL, "xmgn_processor_fwd: null argument");
+    if (part < 0 || part >= (int)ws->g->parts.size())
+      return set_error(XMGN_EINVAL, "xmgn_processor_fwd: part=%d outside [0,%d)", part, (int)ws->g->parts.size());
+    XMGN_CUDA(cudaSetDevice(ws->dev), "xmgn_processor_fwd: cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    const Part& P = ws->g->parts[part];
+    const DPart& dp = ws->dparts[part];
+    const int H = ws->H, L = ws->L, m = ws->m;
+    const long long NH = ws->Nmax * (long long)H, EH = ws->Emax * (long long)H;
+    Layout Ly{H, L, m};
+    launch_pack(params, ws->d_jobs, ws->njobs, st);
+    const int64_t n0 = n_at(P, L, 0), e1 = e_at(P, L, 1);
+    launch_to_bf16(h0, ws->h_ck.p, ws->h_ck.lo, n0 * H, st);
+    launch_to_bf16(e0, ws->e_ck.p, ws->e_ck.lo, e1 * H, st);
+    const int W1 = 0, W2 = 2;  // weight map slots
+    auto r1 = [&](int l, int slot) { return (l * ws->S1 + slot) * H; };
+    auto r2 = [&](int l, int slot) { return (l * ws->S2 + slot) * H; };
+    {  // P = h0 [W1e_s | W1e_d] for layer 1
+      Prog pr;
+      set_a(ws, pr, 4, ws->h_ck, n0, H);
+      for (int half = 0; half < 2; ++half) {
+        Step& s = pr.add();
+        s.a_src = A_TMA; s.a_map0 = 4; s.K = H;
+        s.b_map = W1; s.b_row0 = r1(0, half ? SL_PDT : SL_PST);
+        s.epi = EPI_STORE; s.f_out = ws->P; s.ld_out = 2 * H; s.col0 = half * H;
+      }
+      run_prog(ws, pr, (int)n0, nullptr, nullptr, false, st);
+    }
+    int cur = 0;
+    for (int l = 1; l <= L; ++l) {
+      const int li = l - 1;
+      const int64_t nl = n_at(P, L, l), el = e_at(P, L, l);
+      const float* e_in = l == 1 ? e0 : ws->e_buf[cur];
+      const float* h_in = l == 1 ? h0 : ws->h_buf[cur];
+      float* e_out = ws->e_buf[cur ^ 1];
+      float* hn = l == L ? h_out : ws->h_buf[cur ^ 1];
+      BfBuf eck_prev = at(ws->e_ck, (long long)li * EH), hck_prev = at(ws->h_ck, (long long)li * NH);
+      BfBuf ack = at(ws->a_ck, (long long)li * NH);
+      {  // edge update (Eq. 1)
+        Prog pr;
+        set_a(ws, pr, 4, eck_prev, el, H);
+        for (int j = 0; j < m; ++j) {
+          Step& s = pr.add();
+          s.a_src = j == 0 ? A_TMA : A_ACT; s.a_map0 = 4; s.K = H;
+          s.b_map = W1; s.b_row0 = r1(li, j == 0 ? SL_E1T : SL_EJT + j - 1);
+          s.epi = EPI_SILU; s.bias = params + Ly.b(li, 0, j);
+          if (j == 0) { s.flags |= EF_GATHER_P; s.gather = ws->P; }
+        }
+        Step& s = pr.add();
+        s.a_src = A_ACT; s.K = H; s.b_map = W1; s.b_row0 = r1(li, SL_EJT + m - 1);
+        s.epi = EPI_LN_FWD; s.bias = params + Ly.b(li, 0, m);
+        s.gamma = params + Ly.gamma(li, 0); s.beta = params + Ly.beta(li, 0);
+        s.f_in = e_in; s.ld_in = H; s.f_out = e_out; s.ld_out = H;
+        if (l < L) { s.flags |= EF_STORE_BF; s.bf_out = ws->e_ck.p + (long long)l * EH; s.bf_lo = ws->e_ck.lo; }
+        run_prog(ws, pr, (int)el, dp.src, dp.dst, false, st);
+      }
+      // aggregation (Eq. 2) -> a^l (BF16 operand + checkpoint)
+      launch_aggregate(H, dp.off, e_out, ack.p, ack.lo, (int)nl, st);
+      XMGN_CUDA(cudaGetLastError(), "aggregate launch");
+      {  // node update (Eq. 3) [+ P for layer l+1]
+        Prog pr;
+        set_a(ws, pr, 4, hck_prev, nl, H);
+        set_a(ws, pr, 6, ack, nl, H);
+        for (int j = 0; j < m; ++j) {
+          Step& s = pr.add();
+          s.a_src = j == 0 ? A_TMA : A_ACT; s.a_map0 = 4; s.a_map1 = 6; s.a_ksplit = H;
+          s.K = j == 0 ? 2 * H : H;
+          s.b_map = j == 0 ? W2 : W1; s.b_row0 = j == 0 ? r2(li, SL2_N1T) : r1(li, sl_njt(m) + j - 1);
+          s.epi = EPI_SILU; s.bias = params + Ly.b(li, 1, j);
+        }
+        Step& s = pr.add();
+        s.a_src = A_ACT; s.K = H; s.b_map = W1; s.b_row0 = r1(li, sl_njt(m) + m - 1);
+        s.epi = EPI_LN_FWD; s.bias = params + Ly.b(li, 1, m);
+        s.gamma = params + Ly.gamma(li, 1); s.beta = params + Ly.beta(li, 1);
+        s.f_in = h_in; s.ld_in = H; s.f_out = hn; s.ld_out = H;
+        if (l < L) {
+          s.flags |= EF_STORE_BF | EF_WRITE_ACT;
+          s.bf_out = ws->h_ck.p + (long long)l * NH; s.bf_lo = ws->h_ck.lo;
+          for (int half = 0; half < 2; ++half) {
+            Step& q = pr.add();
+            q.a_src = A_ACT; q.K = H; q.b_map = W1; q.b_row0 = r1(l, half ? SL_PDT : SL_PST);
+            q.epi = EPI_STORE; q.f_out = ws->P; q.ld_out = 2 * H; q.col0 = half * H;
+          }
+        }
+        run_prog(ws, pr, (int)nl, nullptr, nullptr, false, st);
+      }
+      cur ^= 1;
+    }
+    ws->last_fwd = part;
+    return XMGN_OK;
+  });
+}
+
+extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const float* params, const float* grad_h_out,
+                                          float* grad_params, float* grad_h0, float* grad_e0, void* stream) {
+  return guarded("xmgn_processor_bwd", [&]() -> xmgn_status {
+    if (!ws || !params || !grad_h_out || !grad_params)
+      return set_error(XMGN_EINVAL, "xmgn_processor_bwd: null argument");
+    if (part != ws->last_fwd)
+      return set_error(XMGN_ESTATE, "xmgn_processor_bwd: part=%d but the workspace holds the forward of part %d",
+                       part, ws->last_fwd);
+    XMGN_CUDA(cudaSetDevice(ws->dev), "xmgn_processor_bwd: cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    const Part& P = ws->g->parts[part];
+    const DPart& dp = ws->dparts[part];
+    const int H = ws->H, L = ws->L, m = ws->m;
+    const long long NH = ws->Nmax * (long long)H, EH = ws->Emax * (long long)H;
+    Layout Ly{H, L, m};
+    const int W1 = 0, W2 = 2;
+    auto r1 = [&](int l, int slot) { return (l * ws->S1 + slot) * H; };
+    auto r2 = [&](int l, int slot) { return (l * ws->S2 + slot) * H; };
+    launch_pack(params, ws->d_jobs, ws->njobs, st);
+    // seed: dL/dh^L on owned rows (the loss mask of PAPER.md:197 is the prefix)
+    XMGN_CUDA(cudaMemcpyAsync(ws->Gh, grad_h_out, P.n_owned * H * sizeof(float), cudaMemcpyDeviceToDevice, st),
+              "seed copy");
+    const BfBuf none{};
+    for (int l = L; l >= 1; --l) {
+      const int li = l - 1;
+      const int64_t nl = n_at(P, L, l), el = e_at(P, L, l), nprev = n_at(P, L, l - 1);
+      const int64_t enext = l < L ? e_at(P, L, l + 1) : 0;
+      BfBuf eck = at(ws->e_ck, (long long)li * EH), hck = at(ws->h_ck, (long long)li * NH);
+      BfBuf ack = at(ws->a_ck, (long long)li * NH);
+      const int tiles_n = (int)((nl + 127) / 128), tiles_e = (int)((el + 127) / 128);
+      // common recompute + dgrad program of an MLP block (blk 0 edge, 1 node)
+      auto mlp_bwd = [&](Prog& pr, int blk) {
+        for (int j = 0; j < m; ++j) {
+          Step& s = pr.add();
+          s.a_src = j == 0 ? A_TMA : A_ACT; s.a_map0 = 4;
+          if (blk == 1) { s.a_map1 = 6; s.a_ksplit = H; }
+          s.K = (j == 0 && blk == 1) ? 2 * H : H;
+          s.b_map = (j == 0 && blk == 1) ? W2 : W1;
+          s.b_row0 = j == 0 ? (blk ? r2(li, SL2_N1T) : r1(li, SL_E1T))
+                            : r1(li, (blk ? sl_njt(m) : SL_EJT) + j - 1);
+          s.epi = EPI_SILU; s.bias = params + Ly.b(li, blk, j);
+          s.flags = EF_STORE_A | EF_STORE_S;
+          s.scr_a = ws->scrA[j].p; s.scr_s = ws->scrS[j].p; s.lo_off = ws->scrA[j].lo;
+          if (j == 0 && blk == 0) { s.flags |= EF_GATHER_P; s.gather = ws->P; }
+        }
+        Step& s = pr.add();
+        s.a_src = A_ACT; s.K = H; s.b_map = W1; s.b_row0 = r1(li, (blk ? sl_njt(m) : SL_EJT) + m - 1);
+        s.epi = EPI_LN_BWD; s.bias = params + Ly.b(li, blk, m);
+        s.gamma = params + Ly.gamma(li, blk); s.beta = params + Ly.beta(li, blk);
+        s.f_in = blk ? ws->Gh : ws->Ge; s.ld_in = H;
+        s.valid_in = blk ? (int)nl : (int)enext;
+        if (blk == 0) { s.flags |= EF_GATHER_G; s.gather = ws->Ga; }
+        s.scr_z = ws->scrZ[m].p; s.lo_off = ws->scrZ[m].lo;
+        for (int j = m; j >= 1; --j) {
+          Step& d = pr.add();
+          d.a_src = A_ACT; d.K = H; d.b_map = W1; d.b_row0 = r1(li, (blk ? sl_nj(m) : sl_ej(m)) + j - 1);
+          d.epi = EPI_DSILU; d.scr_s = ws->scrS[j - 1].p; d.scr_z = ws->scrZ[j - 1].p; d.lo_off = ws->scrZ[j - 1].lo;
+          d.vec0 = 3 + (m - j);
+        }
+      };
+      {  // node block backward
+        Prog pr;
+        set_a(ws, pr, 4, hck, nl, H);
+        set_a(ws, pr, 6, ack, nl, H);
+        mlp_bwd(pr, 1);
+        Step& a = pr.add();   // dh: G_h += dZ0 W0[h rows]^T
+        a.a_src = A_ACT; a.K = H; a.b_map = W1; a.b_row0 = r1(li, sl_n1h(m));
+        a.epi = EPI_ADD; a.f_in = ws->Gh; a.f_out = ws->Gh; a.ld_in = a.ld_out = H; a.valid_in = (int)nl;
+        Step& b = pr.add();   // da: G_a = dZ0 W0[agg rows]^T
+        b.a_src = A_ACT; b.K = H; b.b_map = W1; b.b_row0 = r1(li, sl_n1a(m));
+        b.epi = EPI_STORE; b.f_out = ws->Ga; b.ld_out = H; b.col0 = 0;
+        run_prog(ws, pr, (int)nl, nullptr, nullptr, true, st);
+        colsum_reduce(ws, 1, li, grad_params, std::min(tiles_n, ws->sms), st);
+        wgrad(ws, hck, ack, H, H / 128, ws->scrZ[0], H, 0, nl, 2 * H, grad_params, Ly.W(li, 1, 0), st);
+        for (int j = 1; j <= m; ++j)
+          wgrad(ws, ws->scrA[j - 1], none, H, H / 128, ws->scrZ[j], H, 0, nl, H, grad_params, Ly.W(li, 1, j), st);
+      }
+      {  // recompute P for layer l from h^{l-1}
+        Prog pr;
+        set_a(ws, pr, 4, hck, nprev, H);
+        for (int half = 0; half < 2; ++half) {
+          Step& s = pr.add();
+          s.a_src = A_TMA; s.a_map0 = 4; s.K = H;
+          s.b_map = W1; s.b_row0 = r1(li, half ? SL_PDT : SL_PST);
+          s.epi = EPI_STORE; s.f_out = ws->P; s.ld_out = 2 * H; s.col0 = half * H;
+        }
+        run_prog(ws, pr, (int)nprev, nullptr, nullptr, false, st);
+      }
+      {  // edge block backward
+        Prog pr;
+        set_a(ws, pr, 4, eck, el, H);
+        mlp_bwd(pr, 0);
+        Step& a = pr.add();   // G_e^{l-1} = G_e' + dZ0 W0[e rows]^T
+        a.a_src = A_ACT; a.K = H; a.b_map = W1; a.b_row0 = r1(li, sl_e1e(m));
+        a.epi = EPI_ADD; a.f_in = ws->Ge; a.f_out = ws->Ge; a.ld_in = a.ld_out = H; a.valid_in = (int)enext;
+        a.flags = EF_GATHER_G; a.gather = ws->Ga;
+        run_prog(ws, pr, (int)el, dp.src, dp.dst, true, st);
+        colsum_reduce(ws, 0, li, grad_params, std::min(tiles_e, ws->sms), st);
+        wgrad(ws, eck, none, H, H / 128, ws->scrZ[0], H, 0, el, H, grad_params, Ly.W(li, 0, 0), st);
+        for (int j = 1; j <= m; ++j)
+          wgrad(ws, ws->scrA[j - 1], none, H, H / 128, ws->scrZ[j], H, 0, el, H, grad_params, Ly.W(li, 0, j), st);
+      }
+      // D = [sum over out-edges | sum over in-edges] of dZ0 (adjoint of the P gathers)
+      launch_segsum(H, dp.off, dp.rev, ws->scrZ[0].p, ws->scrZ[0].lo, ws->D.p, ws->D.lo, (int)nprev, (int)el, st);
+      XMGN_CUDA(cudaGetLastError(), "segsum launch");
+      {  // G_h^{l-1} = [rows < n_l] G_h + D [W_s | W_d]^T
+        Prog pr;
+        set_a(ws, pr, 4, ws->D, nprev, 2 * H);
+        Step& s = pr.add();
+        s.a_src = A_TMA; s.a_map0 = 4; s.K = 2 * H; s.b_map = W2; s.b_row0 = r2(li, SL2_SD);
+        s.epi = EPI_ADD; s.f_in = ws->Gh; s.f_out = ws->Gh; s.ld_in = s.ld_out = H; s.valid_in = (int)nl;
+        run_prog(ws, pr, (int)nprev, nullptr, nullptr, false, st);
+      }
+      // dW_s = h^T D_src, dW_d = h^T D_dst
+      wgrad(ws, hck, none, H, H / 128, ws->D, 2 * H, 0, nprev, H, grad_params, Ly.W(li, 0, 0) + (long long)H * H, st);
+      wgrad(ws, hck, none, H, H / 128, ws->D, 2 * H, H, nprev, H, grad_params, Ly.W(li, 0, 0) + 2LL * H * H, st);
+    }
+    const int64_t n0 = n_at(P, L, 0), e1 = e_at(P, L, 1);
+    if (grad_h0) {
+      XMGN_CUDA(cudaMemcpyAsync(grad_h0, ws->Gh, n0 * H * sizeof(float), cudaMemcpyDeviceToDevice, st), "grad_h0");
+      if (P.n_local > n0)
+        XMGN_CUDA(cudaMemsetAsync(grad_h0 + n0 * H, 0, (P.n_local - n0) * H * sizeof(float), st), "grad_h0");
+    }
+    if (grad_e0) {
+      XMGN_CUDA(cudaMemcpyAsync(grad_e0, ws->Ge, e1 * H * sizeof(float), cudaMemcpyDeviceToDevice, st), "grad_e0");
+      if (P.e_local > e1)
+        XMGN_CUDA(cudaMemsetAsync(grad_e0 + e1 * H, 0, (P.e_local - e1) * H * sizeof(float), st), "grad_e0");
+    }
+    return XMGN_OK;
+  });
+}
+
+extern "C" xmgn_status xmgn_check_finite(const float* dev, size_t n, void* stream) {
+  return guarded("xmgn_check_finite", [&]() -> xmgn_status {
+    cudaStream_t st = (cudaStream_t)stream;
+    int* flag = nullptr;
+    XMGN_CUDA(cudaMallocAsync((void**)&flag, 4, st), "xmgn_check_finite");
+    XMGN_CUDA(cudaMemsetAsync(flag, 0, 4, st), "xmgn_check_finite");
+    launch_nonfinite(dev, (long long)n, flag, st);
+    int h = 0;
+    XMGN_CUDA(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, st), "xmgn_check_finite");
+    XMGN_CUDA(cudaStreamSynchronize(st), "xmgn_check_finite");
+    cudaFreeAsync(flag, st);
+    if (h) return set_error(XMGN_ENONFINITE, "xmgn_check_finite: non-finite value among %zu floats", n);
+    return XMGN_OK;
+  });
+}

@@ -1,0 +1,223 @@
+"""Thin ctypes binding of libxmgn.so (include/xmgn.h) -- argument marshalling only.
+
+Every step of the processor runs in the CUDA library; this module converts
+numpy / torch arguments to pointers and status codes to exceptions.  There is
+no fallback: if libxmgn.so is missing the import fails.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libxmgn.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+_lib = ctypes.CDLL(LIB_PATH)
+
+PREC_BF16, PREC_FP32_CHECK = 0, 1
+STATUS = {0: "OK", 1: "EINVAL", 2: "EHALO", 3: "ESTATE", 4: "ENOMEM", 5: "ECUDA", 6: "ENCCL",
+          7: "ENONFINITE", 8: "EUNSUPPORTED"}
+
+
+class XmgnError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = STATUS.get(status, status)
+
+
+_vp, _i64, _i32, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+
+
+class GraphDesc(ctypes.Structure):
+    _fields_ = [("n_nodes", _i64), ("n_edges", _i64), ("csr_offsets", _vp), ("csr_sources", _vp),
+                ("n_parts", ctypes.c_int32), ("halo_depth", ctypes.c_int32), ("owned_offsets", _vp),
+                ("owned", _vp), ("halo_offsets", _vp), ("halo", _vp), ("halo_ring", _vp)]
+
+
+class PartInfo(ctypes.Structure):
+    _fields_ = [("n_owned", _i64), ("n_local", _i64), ("e_local", _i64), ("depth", ctypes.c_int32),
+                ("ring_nodes", _i64 * 65), ("ring_edges", _i64 * 65)]
+
+
+class ModelCfg(ctypes.Structure):
+    _fields_ = [("hidden", ctypes.c_int32), ("layers", ctypes.c_int32), ("mlp_hidden_layers", ctypes.c_int32),
+                ("precision", ctypes.c_int32), ("ln_eps", ctypes.c_float)]
+
+
+def _sig(name, res, args):
+    f = getattr(_lib, name)
+    f.restype, f.argtypes = res, args
+    return f
+
+
+_sig("xmgn_last_error", ctypes.c_char_p, [])
+_sig("xmgn_version", ctypes.c_char_p, [])
+_sig("xmgn_load_graph", _i32, [ctypes.POINTER(GraphDesc), _i32, ctypes.POINTER(_vp)])
+_sig("xmgn_part_info_get", _i32, [_vp, _i32, ctypes.POINTER(PartInfo)])
+_sig("xmgn_export_part", _i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp])
+_sig("xmgn_free_graph", None, [_vp])
+_sig("xmgn_param_count", _sz, [ctypes.POINTER(ModelCfg)])
+_sig("xmgn_workspace_create", _i32, [_vp, ctypes.POINTER(ModelCfg), ctypes.POINTER(_vp)])
+_sig("xmgn_workspace_bytes", _sz, [_vp])
+_sig("xmgn_workspace_free", None, [_vp])
+_sig("xmgn_processor_fwd", _i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp])
+_sig("xmgn_processor_bwd", _i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp])
+_sig("xmgn_check_finite", _i32, [_vp, _sz, _vp])
+_sig("xmgn_comm_unique_id", _i32, [ctypes.c_char_p])
+_sig("xmgn_comm_init", _i32, [ctypes.c_char_p, _i32, _i32, _i32, ctypes.POINTER(_vp)])
+_sig("xmgn_grad_reduce", _i32, [_vp, _vp, _sz, _vp])
+_sig("xmgn_comm_destroy", None, [_vp])
+_sig("xmgn_selftest_gemm", _i32, [_i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp])
+
+EXPORTS = ["xmgn_last_error", "xmgn_version", "xmgn_load_graph", "xmgn_part_info_get", "xmgn_export_part",
+           "xmgn_free_graph", "xmgn_param_count", "xmgn_workspace_create", "xmgn_workspace_bytes",
+           "xmgn_workspace_free", "xmgn_processor_fwd", "xmgn_processor_bwd", "xmgn_check_finite",
+           "xmgn_comm_unique_id", "xmgn_comm_init", "xmgn_grad_reduce", "xmgn_comm_destroy",
+           "xmgn_selftest_gemm"]
+
+
+def _check(status):
+    if status != 0:
+        raise XmgnError(status, _lib.xmgn_last_error().decode(errors="replace"))
+
+
+def version():
+    return _lib.xmgn_version().decode()
+
+
+def _ptr(x):
+    """Device/host pointer of a torch tensor or numpy array (None -> NULL)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+def _stream(s):
+    if s is None:
+        return None
+    return getattr(s, "cuda_stream", s)
+
+
+def _i64c(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+class Graph:
+    """xmgn_load_graph: CSR by destination + per-partition owned / halo lists."""
+
+    def __init__(self, offsets, sources, owned_offsets, owned, halo_offsets, halo, halo_ring, halo_depth,
+                 device=0):
+        self._keep = [_i64c(offsets), _i64c(sources), _i64c(owned_offsets), _i64c(owned), _i64c(halo_offsets),
+                      _i64c(halo), np.ascontiguousarray(halo_ring, dtype=np.int32)]
+        o, s, oo, ow, ho, ha, hr = self._keep
+        d = GraphDesc(len(o) - 1, len(s), o.ctypes.data, s.ctypes.data, len(oo) - 1, int(halo_depth),
+                      oo.ctypes.data, ow.ctypes.data, ho.ctypes.data, ha.ctypes.data, hr.ctypes.data)
+        h = _vp()
+        _check(_lib.xmgn_load_graph(ctypes.byref(d), int(device), ctypes.byref(h)))
+        self.handle = h
+        self.n_parts = len(oo) - 1
+        self._keep = None
+
+    @classmethod
+    def from_bundle(cls, b, halo_depth, device=0):
+        return cls(b["offsets"], b["sources"], b["owned_offsets"], b["owned"], b["halo_offsets"], b["halo"],
+                   b["halo_ring"], halo_depth, device)
+
+    def part_info(self, p):
+        pi = PartInfo()
+        _check(_lib.xmgn_part_info_get(self.handle, int(p), ctypes.byref(pi)))
+        d = pi.depth
+        return dict(n_owned=pi.n_owned, n_local=pi.n_local, e_local=pi.e_local, depth=d,
+                    ring_nodes=list(pi.ring_nodes[:d + 2]), ring_edges=list(pi.ring_edges[:d + 2]))
+
+    def export(self, p):
+        info = self.part_info(p)
+        n, e = info["n_local"], info["e_local"]
+        out = dict(gid=np.empty(n, np.int64), offsets=np.empty(n + 1, np.int64), sources=np.empty(e, np.int64),
+                   edge_gid=np.empty(e, np.int64), rev=np.empty(e, np.int64))
+        _check(_lib.xmgn_export_part(self.handle, int(p), out["gid"].ctypes.data, out["offsets"].ctypes.data,
+                                     out["sources"].ctypes.data, out["edge_gid"].ctypes.data,
+                                     out["rev"].ctypes.data))
+        out.update(info)
+        return out
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.xmgn_free_graph(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.close()
+
+
+def model_cfg(hidden, layers, m=2, precision=PREC_BF16, ln_eps=1e-5):
+    return ModelCfg(hidden, layers, m, precision, ln_eps)
+
+
+def param_count(cfg):
+    return int(_lib.xmgn_param_count(ctypes.byref(cfg)))
+
+
+class Workspace:
+    """xmgn_workspace_create / processor_fwd / processor_bwd for one GPU."""
+
+    def __init__(self, graph, cfg):
+        self.graph, self.cfg = graph, cfg
+        h = _vp()
+        _check(_lib.xmgn_workspace_create(graph.handle, ctypes.byref(cfg), ctypes.byref(h)))
+        self.handle = h
+
+    def nbytes(self):
+        return int(_lib.xmgn_workspace_bytes(self.handle))
+
+    def forward(self, part, params, h0, e0, h_out, stream=None):
+        _check(_lib.xmgn_processor_fwd(self.handle, int(part), _ptr(params), _ptr(h0), _ptr(e0), _ptr(h_out),
+                                       _stream(stream)))
+
+    def backward(self, part, params, grad_h_out, grad_params, grad_h0=None, grad_e0=None, stream=None):
+        _check(_lib.xmgn_processor_bwd(self.handle, int(part), _ptr(params), _ptr(grad_h_out),
+                                       _ptr(grad_params), _ptr(grad_h0), _ptr(grad_e0), _stream(stream)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.xmgn_workspace_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.close()
+
+
+def check_finite(t, stream=None):
+    _check(_lib.xmgn_check_finite(_ptr(t), t.numel(), _stream(stream)))
+
+
+class Comm:
+    """NCCL communicator for xmgn_grad_reduce (one per process / GPU)."""
+
+    @staticmethod
+    def unique_id():
+        buf = ctypes.create_string_buffer(128)
+        _check(_lib.xmgn_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, uid, nranks, rank, device):
+        h = _vp()
+        _check(_lib.xmgn_comm_init(bytes(uid), int(nranks), int(rank), int(device), ctypes.byref(h)))
+        self.handle = h
+
+    def grad_reduce(self, grad, stream=None):
+        _check(_lib.xmgn_grad_reduce(self.handle, _ptr(grad), grad.numel(), _stream(stream)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.xmgn_comm_destroy(self.handle)
+            self.handle = None
+
+
+def selftest_gemm(A, B, C, a_mn_major, b_mn_major, M, N, K, stream=None):
+    _check(_lib.xmgn_selftest_gemm(M, N, K, int(a_mn_major), int(b_mn_major), _ptr(A), _ptr(B), _ptr(C),
+                                   _stream(stream)))
