@@ -1,0 +1,379 @@
+"""Benchmark: partitioned X-MeshGraphNet processor fwd+bwd (15 layers) on B200.
+
+Metric (BASELINE.json): processor edges/s fwd+bwd (15 layers) at 1/2/4/8 B200,
+with the dominant kernel's roofline fraction.  Workload: CFG4 -- the 2M-point
+3-level (500k/1M/2M) car-proxy cloud, k=6, H=512, L=15, m=2,
+8 RCB partitions with halo 15, spread over the ranks in contiguous blocks.
+
+One step = fwd + bwd of every partition of this rank (gradients summed in
+partition order) + one NCCL all-reduce of the flat FP32 gradient
+(xmgn_grad_reduce) when N > 1.  value = global unique directed edges x ranks'
+steps / max-over-ranks device time.  Inputs (h0, e0, g per partition) are
+generated on the device before the timed region; every per-partition tensor is
+far larger than L2 (e0 alone is ~6.6 GB), so no explicit flush is needed.
+
+--impl reference: the FP64 CPU oracle (oracle/, the tier's reference arm) on a
+bounded sample of the same workload, rank 0 only.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+H, L, M_HID = 512, 15, 2
+METRIC = "processor edges/s fwd+bwd (15 layers)"
+
+
+def assign_parts(P, world, rank):
+    """Contiguous blocks of partitions per rank (RCB order), SURVEY §8(e)."""
+    return list(range(rank * P // world, (rank + 1) * P // world))
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- CPU oracle sample
+def oracle_sample(bundle, target_edges, H_=H, L_=L, m=M_HID):
+    """A connected subgraph of the workload (BFS ball around node 0 grown until it
+    holds >= target_edges local edges) as a single owned set: returns its CSR."""
+    import oracle
+    off, src = bundle["offsets"], bundle["sources"]
+    seed = np.array([int(bundle["owned"][0])])
+    for depth in range(1, 40):
+        lg = oracle.local_graph(off, src, seed, depth)
+        if len(lg["sources"]) >= target_edges:
+            break
+    return lg
+
+
+def time_oracle(lg, H_=H, L_=L, m=M_HID, reps=1):
+    import oracle
+    from xmgn_inputs import tensors
+    P = tensors.params(H_, L_, m).double().numpy()
+    h0 = tensors.node_features(lg["gid"], H_).double().numpy()
+    e0 = tensors.edge_features(lg["edge_gid"], H_).double().numpy()
+    g = tensors.upstream_grad(lg["gid"], H_).double().numpy()
+    ts = []
+    for _ in range(reps):
+        t = time.perf_counter()
+        f = oracle.forward(lg["offsets"], lg["sources"], P, h0, e0, H_, L_, m)
+        oracle.backward(lg["offsets"], lg["sources"], P, f, g, H_, L_, m)
+        ts.append(time.perf_counter() - t)
+    return ts
+
+
+def cpu_cores():
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    def __init__(self, device):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+        self.device = device
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- algorithmic work per scope
+def scope_work(info, H_=H, L_=L, m=M_HID):
+    """Algorithmic FLOPs (MMA work the method needs; recompute excluded) and
+    executed FLOPs per launch scope for one fwd+bwd of one partition, plus the
+    aggregation's algorithmic bytes.  Rows per layer follow halo shrinking."""
+    rn, re_ = info["ring_nodes"], info["ring_edges"]
+    n_at = lambda l: rn[L_ - l + 1]  # noqa: E731
+    e_at = lambda l: re_[L_ - l + 1]  # noqa: E731
+    H2 = H_ * H_
+    w = {}
+
+    def add(k, alg, exe=None):
+        a, e = w.get(k, (0.0, 0.0))
+        w[k] = (a + alg, e + (alg if exe is None else exe))
+    add("chain_proj", 2 * 2 * H2 * n_at(0))                       # fwd P for layer 1
+    for l in range(1, L_ + 1):
+        nl, el, npv = n_at(l), e_at(l), n_at(l - 1)
+        add("chain_edge_fwd", 2 * (1 + m) * H2 * el)
+        add("chain_node_fwd", 2 * ((2 + m) * H2 + (2 * H2 if l < L_ else 0)) * nl)
+        add("aggregate", 0)
+        fw_e, fw_n = 2 * (1 + m) * H2 * el, 2 * (2 + m) * H2 * nl
+        add("chain_node_bwd", 2 * (m + 2) * H2 * nl, fw_n + 2 * (m + 2) * H2 * nl)
+        add("chain_edge_bwd", 2 * (m + 1) * H2 * el, fw_e + 2 * (m + 1) * H2 * el)
+        add("chain_proj", 0, 2 * 2 * H2 * npv)                      # recompute P in bwd
+        add("chain_projbwd", 2 * 2 * H2 * npv)
+        add("wgrad", 2 * ((2 + m) * H2 * nl + (1 + m) * H2 * el + 2 * H2 * npv))
+    agg_bytes = sum(4 * H_ * e_at(l) + 2 * H_ * n_at(l) for l in range(1, L_ + 1))
+    return w, agg_bytes
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="xmgn", choices=["xmgn", "reference"])
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    from xmgn_inputs import configs
+    from paper_2411_17164_b200 import xmgn
+    from paper_2411_17164_b200.processor import Processor
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = configs.CONFIGS[args.config]
+    Hc, Lc = cfg["H"], cfg["L"]
+    # rank 0 builds (and caches) the graph, the others read the cache
+    if world > 1 and rank != 0:
+        dist.barrier()
+    t_gen = time.time()
+    bundle = configs.load(args.config)
+    t_gen = time.time() - t_gen
+    if world > 1 and rank == 0:
+        dist.barrier()
+    P = len(bundle["owned_offsets"]) - 1
+    parts = assign_parts(P, world, rank)
+    prec = xmgn.PREC_FP16 if args.precision == "fp16" else xmgn.PREC_BF16
+    pr = Processor(bundle, Hc, Lc, m=M_HID, precision=prec, device=local, parts=parts, halo_depth=Lc)
+    E_global = int(len(bundle["sources"]))
+    params = pr.make_params()
+    grad = torch.zeros(pr.n_params, device=dev)
+    inputs = {p: pr.make_inputs(p) for p in parts}
+    comm = None
+    if world > 1:
+        uid = [xmgn.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = xmgn.Comm(uid[0], world, rank, local)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        grad.zero_()
+        pr.step(params, grad, inputs, stream)
+        if comm is not None:
+            comm.grad_reduce(grad, stream)
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    sync_all()
+    xmgn.profile_enable(True)
+    xmgn.profile_collect()
+    l0 = xmgn.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        sync_all()
+    launches = xmgn.launch_count() - l0
+    xmgn.profile_enable(False)
+    prof = xmgn.profile_collect()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = E_global / (ms / 1e3)
+    clocks = clk.summary()
+    xmgn.check_finite(grad)
+
+    # ---- roofline of the dominant kernel scope (this rank's live CUDA-event timings)
+    work = {}
+    agg_bytes = 0
+    for p in parts:
+        w, ab = scope_work(pr.info[p], Hc, Lc, M_HID)
+        agg_bytes += ab
+        for k, (a, e) in w.items():
+            A, Ee = work.get(k, (0.0, 0.0))
+            work[k] = (A + a, Ee + e)
+    pk = peaks() or {}
+    dom = max(prof, key=lambda k: prof[k][0]) if prof else None
+    roof = None
+    if dom:
+        tot_ms, n_launch = prof[dom]
+        per_launch_s = tot_ms / 1e3 / n_launch
+        if dom == "aggregate":
+            achieved = agg_bytes * args.steps / n_launch / per_launch_s / 1e9
+            peak, unit, bound, src = pk.get("hbm_gbs", 6650.0), "GB/s", "hbm", "measured" if pk else "fallback"
+        else:
+            alg = work.get(dom, (0.0, 0.0))[0] * args.steps / n_launch
+            achieved = alg / per_launch_s / 1e12
+            peak = pk.get("bf16_tflops_sustained", 1400.0)
+            unit, bound, src = "TFLOP/s", "tensor", "measured sustained bf16 (fp16 same nominal rate)"
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tf):
+            traffic = json.load(open(tf)).get(dom)
+        roof = {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom, "peak_source": src,
+                "launches": n_launch, "avg_launch_ms": round(tot_ms / n_launch, 4),
+                "share_of_step": round(tot_ms / (ms * args.steps), 4)}
+        exe = work.get(dom, (0.0, 0.0))[1] * args.steps / n_launch
+        if exe and dom != "aggregate":
+            roof["executed_tflops"] = round(exe / per_launch_s / 1e12, 2)
+    scopes = {k: {"ms_per_step": round(v[0] / args.steps, 3), "launches_per_step": v[1] / args.steps}
+              for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    total_alg = sum(a for a, _ in work.values())
+    t2 = torch.tensor([total_alg], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t2)
+
+    # ---- e2e through the public API with host buffers (H2D inputs, D2H result)
+    e2e = None
+    if not args.no_e2e:
+        host = {}
+        for p in parts:
+            host[p] = [x.cpu().pin_memory() for x in inputs[p]]
+        dev_in = {p: [torch.empty_like(x) for x in inputs[p]] for p in parts}
+        grad_host = torch.empty(pr.n_params, dtype=torch.float32).pin_memory()
+        bi = sum(x.numel() * 4 for p in parts for x in host[p])
+        bo = grad_host.numel() * 4
+
+        def e2e_step():
+            for p in parts:
+                for d_, h_ in zip(dev_in[p], host[p]):
+                    d_.copy_(h_, non_blocking=True)
+            grad.zero_()
+            pr.step(params, grad, dev_in, stream)
+            if comm is not None:
+                comm.grad_reduce(grad, stream)
+            grad_host.copy_(grad, non_blocking=True)
+
+        e2e_step()
+        sync_all()
+        k2 = max(1, min(args.steps, 2))
+        ev0.record(stream)
+        for _ in range(k2):
+            e2e_step()
+        ev1.record(stream)
+        sync_all()
+        ms2 = ev0.elapsed_time(ev1) / k2
+        t3 = torch.tensor([ms2], device=dev)
+        if world > 1:
+            dist.all_reduce(t3, op=dist.ReduceOp.MAX)
+        e2e = {"value": E_global / (float(t3.item()) / 1e3), "unit": "edges/s", "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": bo, "steps": k2}
+        del host, dev_in
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        lg = oracle_sample(bundle, 2500)
+        ts = time_oracle(lg, Hc, Lc)
+        cpu = {"value": len(lg["sources"]) / ts[0], "unit": "edges/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": f"FP64 oracle fwd+bwd, {Lc} layers, H={Hc}, on a {len(lg['sources'])}-edge "
+                         f"{len(lg['gid'])}-node BFS ball of the {args.config} graph ({ts[0]:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg['levels']} points, k={cfg['k']}, H={Hc}, L={Lc}, "
+                                   f"m={M_HID}, {P} halo partitions (depth {Lc})",
+                       "edges_global": E_global, "partitions": P, "partitions_per_gpu": len(parts),
+                       "parallelism": f"halo-partition dp{world}", "l2": "inputs larger than L2 (no flush)",
+                       "graph_build_s": round(t_gen, 1)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+            "alg_tflops_per_s": round(float(t2.item()) * args.steps / (ms * args.steps / 1e3) / 1e12, 2),
+            "scopes": scopes,
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    pr.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def reference(args, world, rank):
+    """Reference arm: the FP64 oracle as it stands, on host cores, bounded samples."""
+    if rank != 0:
+        return
+    from xmgn_inputs import configs
+    cfg = configs.CONFIGS[args.config]
+    bundle = configs.load(args.config)
+    lg = oracle_sample(bundle, 600)
+    for _ in range(args.warmup):
+        time_oracle(lg, cfg["H"], cfg["L"])
+    ts = time_oracle(lg, cfg["H"], cfg["L"], reps=args.steps)
+    s = sum(ts) / len(ts)
+    v = len(lg["sources"]) / s
+    sample = (f"FP64 oracle fwd+bwd, {cfg['L']} layers, H={cfg['H']}, on a {len(lg['sources'])}-edge "
+              f"{len(lg['gid'])}-node BFS ball of the {args.config} graph per step")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": s * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} (bounded sample)", "parallelism": "host cores"},
+            "cpu_baseline": {"value": v, "unit": "edges/s", "cores": cpu_cores(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -107,9 +107,12 @@ void xmgn_free_graph(xmgn_graph* g);
  *            FP32 residual streams / LN / SiLU / aggregation (PAPER.md:234 AMP).
  *            XMGN_PREC_FP32_CHECK -- every GEMM operand split hi+lo in BF16 and
  *            multiplied as hi*hi + lo*hi + hi*lo (FP32-class products) for the
- *            1e-4 check mode (north_star); H <= 256 only.
+ *            1e-4 check mode (north_star); H = 128 only.
+ *            XMGN_PREC_FP16 -- as BF16 but with FP16 tensor-core operands (same
+ *            MMA rate, 3 more mantissa bits); the mode that meets the 2e-2 x RMS
+ *            bound at 15 layers.
  * mlp_hidden_layers m in {1, 2}; hidden H in {128, 256, 512}.                  */
-enum { XMGN_PREC_BF16 = 0, XMGN_PREC_FP32_CHECK = 1 };
+enum { XMGN_PREC_BF16 = 0, XMGN_PREC_FP32_CHECK = 1, XMGN_PREC_FP16 = 2 };
 typedef struct {
   int32_t hidden, layers, mlp_hidden_layers, precision;
   float ln_eps;
@@ -155,6 +158,16 @@ void xmgn_comm_destroy(xmgn_comm* comm);
  * N in {64,128,256}.  Exercises the descriptor conventions of every kernel.  */
 xmgn_status xmgn_selftest_gemm(int M, int N, int K, int a_mn_major, int b_mn_major, const void* A,
                                const void* B, float* C, void* stream);
+/* Number of kernels this library has launched since load (monotone).        */
+long long xmgn_launch_count(void);
+/* When on, named launch scopes (chain_edge_fwd, chain_edge_bwd, aggregate,
+ * wgrad, ...) are bracketed by CUDA events on their stream.  collect
+ * synchronises on the recorded events and returns, per scope name (names
+ * '\n'-separated in `names`), the summed milliseconds and the launch count;
+ * it then clears the records.                                                */
+xmgn_status xmgn_profile_enable(int on);
+xmgn_status xmgn_profile_collect(char* names, size_t names_len, double* ms, long long* counts, int max,
+                                 int* n_out);
 
 #ifdef __cplusplus
 }

@@ -4,10 +4,10 @@
 
 namespace xmgn {
 
-template <int H, bool SPLIT, bool BWD>
+template <int H, bool SPLIT, bool BWD, bool F16>
 static void chain_launch(const ChainParams& p, int grid, cudaStream_t st) {
   using C = ChainCfg<H, SPLIT>;
-  auto kern = k_chain<H, SPLIT, BWD>;
+  auto kern = k_chain<H, SPLIT, BWD, F16>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
@@ -22,15 +22,22 @@ size_t chain_smem(int H, bool split) {
   return ChainCfg<512, false>::SMEM_BYTES;
 }
 
-void launch_chain(int H, bool split, bool bwd, const ChainParams& p, int grid, cudaStream_t st) {
-  if (H == 128) {
-    if (split) { if (bwd) chain_launch<128, true, true>(p, grid, st); else chain_launch<128, true, false>(p, grid, st); }
-    else { if (bwd) chain_launch<128, false, true>(p, grid, st); else chain_launch<128, false, false>(p, grid, st); }
-  } else if (H == 256) {
-    if (bwd) chain_launch<256, false, true>(p, grid, st); else chain_launch<256, false, false>(p, grid, st);
-  } else {
-    if (bwd) chain_launch<512, false, true>(p, grid, st); else chain_launch<512, false, false>(p, grid, st);
+template <int H, bool F16>
+static void launch_h(bool bwd, const ChainParams& p, int grid, cudaStream_t st) {
+  if (bwd) chain_launch<H, false, true, F16>(p, grid, st);
+  else chain_launch<H, false, false, F16>(p, grid, st);
+}
+
+void launch_chain(int H, bool split, bool f16, bool bwd, const ChainParams& p, int grid, cudaStream_t st) {
+  count_launch();
+  if (split) {  // FP32 check mode: BF16 hi/lo operands, H = 128
+    if (bwd) chain_launch<128, true, true, false>(p, grid, st);
+    else chain_launch<128, true, false, false>(p, grid, st);
+    return;
   }
+  if (H == 128) { if (f16) launch_h<128, true>(bwd, p, grid, st); else launch_h<128, false>(bwd, p, grid, st); }
+  else if (H == 256) { if (f16) launch_h<256, true>(bwd, p, grid, st); else launch_h<256, false>(bwd, p, grid, st); }
+  else { if (f16) launch_h<512, true>(bwd, p, grid, st); else launch_h<512, false>(bwd, p, grid, st); }
 }
 
 }  // namespace xmgn

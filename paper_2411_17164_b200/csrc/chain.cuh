@@ -120,7 +120,7 @@ __device__ __forceinline__ float sigmoid_(float v) {
 
 // Store 32 consecutive values (cols c0..c0+31) of row `row` into a swizzled
 // K-major BF16 tile [H/64 blocks][128 rows][64]; lo = residual in SPLIT mode.
-template <int H, bool SPLIT>
+template <int H, bool SPLIT, bool F16>
 __device__ __forceinline__ void store_tile32(uint8_t* tile, uint32_t lo_off, int row, int c0, const float* v) {
   uint8_t* blk = tile + (c0 >> 6) * (128 * 128);
   const int q0 = (c0 & 63) >> 3;
@@ -128,15 +128,7 @@ __device__ __forceinline__ void store_tile32(uint8_t* tile, uint32_t lo_off, int
   for (int q = 0; q < 4; ++q) {
     uint32_t hi[4], lo[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float a = v[q * 8 + 2 * i], b = v[q * 8 + 2 * i + 1];
-      __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
-      hi[i] = *reinterpret_cast<uint32_t*>(&h2);
-      if constexpr (SPLIT) {
-        float ra = a - __bfloat162float(h2.x), rb = b - __bfloat162float(h2.y);
-        lo[i] = pack_bf16(ra, rb);
-      }
-    }
+    for (int i = 0; i < 4; ++i) split2<F16, SPLIT>(v[q * 8 + 2 * i], v[q * 8 + 2 * i + 1], hi[i], lo[i]);
     uint32_t off = sw128_off(row, q0 + q);
     *reinterpret_cast<uint4*>(blk + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
     if constexpr (SPLIT) *reinterpret_cast<uint4*>(blk + lo_off + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
@@ -144,35 +136,29 @@ __device__ __forceinline__ void store_tile32(uint8_t* tile, uint32_t lo_off, int
 }
 
 // 32 values -> global BF16 row segment (hi, and lo at +lo_off elements in SPLIT).
-template <bool SPLIT>
+template <bool SPLIT, bool F16>
 __device__ __forceinline__ void store_bf32(__nv_bfloat16* p, long long lo_off, const float* v) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint32_t hi[4], lo[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float a = v[q * 8 + 2 * i], b = v[q * 8 + 2 * i + 1];
-      __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
-      hi[i] = *reinterpret_cast<uint32_t*>(&h2);
-      if constexpr (SPLIT) lo[i] = pack_bf16(a - __bfloat162float(h2.x), b - __bfloat162float(h2.y));
-    }
+    for (int i = 0; i < 4; ++i) split2<F16, SPLIT>(v[q * 8 + 2 * i], v[q * 8 + 2 * i + 1], hi[i], lo[i]);
     reinterpret_cast<uint4*>(p)[q] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
     if constexpr (SPLIT) reinterpret_cast<uint4*>(p + lo_off)[q] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
   }
 }
-template <bool SPLIT>
+template <bool SPLIT, bool F16>
 __device__ __forceinline__ void load_bf32(const __nv_bfloat16* p, long long lo_off, float* v) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint4 u = reinterpret_cast<const uint4*>(p)[q];
-    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[q * 8 + i] = __bfloat162float(b[i]);
+    unpack8<F16>(u, v + q * 8);
     if constexpr (SPLIT) {
       uint4 w = reinterpret_cast<const uint4*>(p + lo_off)[q];
-      const __nv_bfloat16* c = reinterpret_cast<const __nv_bfloat16*>(&w);
+      float t[8];
+      unpack8<false>(w, t);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[q * 8 + i] += __bfloat162float(c[i]);
+      for (int i = 0; i < 8; ++i) v[q * 8 + i] += t[i];
     }
   }
 }
@@ -206,7 +192,7 @@ __device__ __forceinline__ float warp_colsum32(float* v) {
   return v[0];
 }
 
-template <int H, bool SPLIT, bool BWD>
+template <int H, bool SPLIT, bool BWD, bool F16>
 __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainParams p) {
   using C = ChainCfg<H, SPLIT>;
   constexpr int F = C::F;
@@ -287,7 +273,7 @@ __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainP
     }
   } else if (w == 1) {
     // ============================ MMA issuer
-    constexpr uint32_t idesc = idesc_bf16(NB, false, false);
+    constexpr uint32_t idesc = idesc_bf16(NB, false, false, F16);
     int ai = 0, bi = 0, g = 0, nact = 0, nidle = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       for (int s = 0; s < p.n_steps; ++s, ++g) {
@@ -396,9 +382,9 @@ __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainP
               sv[i] = x * sg;
               dv[i] = sg * (1.0f + x * (1.0f - sg));
             }
-            store_tile32<H, SPLIT>(act, C::ACT_HALF, trow, c0, sv);
-            if (valid && (st.flags & EF_STORE_A)) store_bf32<SPLIT>(st.scr_a + (size_t)r * H + c0, st.lo_off, sv);
-            if (valid && (st.flags & EF_STORE_S)) store_bf32<SPLIT>(st.scr_s + (size_t)r * H + c0, st.lo_off, dv);
+            store_tile32<H, SPLIT, F16>(act, C::ACT_HALF, trow, c0, sv);
+            if (valid && (st.flags & EF_STORE_A)) store_bf32<SPLIT, F16>(st.scr_a + (size_t)r * H + c0, st.lo_off, sv);
+            if (valid && (st.flags & EF_STORE_S)) store_bf32<SPLIT, F16>(st.scr_s + (size_t)r * H + c0, st.lo_off, dv);
           }
           wrote_act = true;
         } else if (st.epi == EPI_LN_FWD || st.epi == EPI_LN_BWD) {
@@ -436,9 +422,9 @@ __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainP
               }
               if (valid) {
                 store_f32x32(st.f_out + (size_t)r * st.ld_out + c0, v);
-                if (st.flags & EF_STORE_BF) store_bf32<SPLIT>(st.bf_out + (size_t)r * H + c0, st.bf_lo, v);
+                if (st.flags & EF_STORE_BF) store_bf32<SPLIT, F16>(st.bf_out + (size_t)r * H + c0, st.bf_lo, v);
               }
-              if (st.flags & EF_WRITE_ACT) store_tile32<H, SPLIT>(act, C::ACT_HALF, trow, c0, v);
+              if (st.flags & EF_WRITE_ACT) store_tile32<H, SPLIT, F16>(act, C::ACT_HALF, trow, c0, v);
             }
             wrote_act = (st.flags & EF_WRITE_ACT) != 0;
           } else if constexpr (BWD) {
@@ -496,8 +482,8 @@ __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainP
                 float dxh = dy[i] * __ldg(st.gamma + c0 + i);
                 v[i] = valid ? rstd * (dxh - s1 - xh * s2) : 0.f;
               }
-              store_tile32<H, SPLIT>(act, C::ACT_HALF, trow, c0, v);
-              if (valid) store_bf32<SPLIT>(st.scr_z + (size_t)r * H + c0, st.lo_off, v);
+              store_tile32<H, SPLIT, F16>(act, C::ACT_HALF, trow, c0, v);
+              if (valid) store_bf32<SPLIT, F16>(st.scr_z + (size_t)r * H + c0, st.lo_off, v);
               colacc[2][cc] += warp_colsum32(v);    // db_{m+1}
             }
             wrote_act = true;
@@ -509,11 +495,11 @@ __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainP
               const int c0 = cc * 32;
               tmem_ld32(tl + c0, v);
               float sd[32];
-              if (valid) load_bf32<SPLIT>(st.scr_s + (size_t)r * H + c0, st.lo_off, sd);
+              if (valid) load_bf32<SPLIT, F16>(st.scr_s + (size_t)r * H + c0, st.lo_off, sd);
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = valid ? v[i] * sd[i] : 0.f;
-              store_tile32<H, SPLIT>(act, C::ACT_HALF, trow, c0, v);
-              if (valid) store_bf32<SPLIT>(st.scr_z + (size_t)r * H + c0, st.lo_off, v);
+              store_tile32<H, SPLIT, F16>(act, C::ACT_HALF, trow, c0, v);
+              if (valid) store_bf32<SPLIT, F16>(st.scr_z + (size_t)r * H + c0, st.lo_off, v);
               const float cs = warp_colsum32(v);
               if (st.vec0 == 3) colacc[3][cc] += cs;  // db_m
               else colacc[4][cc] += cs;               // db_{m-1}

@@ -31,9 +31,10 @@ static xmgn_status validate_csr(const xmgn_graph_desc* d) {
   if (off[N] != E)
     return set_error(XMGN_EINVAL, "xmgn_load_graph: csr_offsets[%lld]=%lld != n_edges=%lld", (long long)N,
                      (long long)off[N], (long long)E);
-  for (int64_t i = 0; i < N; ++i) {
+  for (int64_t i = 0; i < N; ++i)
     if (off[i + 1] < off[i])
       return set_error(XMGN_EINVAL, "xmgn_load_graph: csr_offsets not monotone at index %lld", (long long)i);
+  for (int64_t i = 0; i < N; ++i) {
     for (int64_t k = off[i]; k < off[i + 1]; ++k) {
       int64_t j = src[k];
       if (j < 0 || j >= N)

@@ -8,6 +8,7 @@
 namespace xmgn {
 
 // ---------------------------------------------------------------- weight packing
+template <bool F16>
 __global__ void k_pack(const float* __restrict__ params, const PackJob* __restrict__ jobs, int njobs) {
   for (int j = 0; j < njobs; ++j) {
     const PackJob J = jobs[j];
@@ -15,14 +16,19 @@ __global__ void k_pack(const float* __restrict__ params, const PackJob* __restri
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
       const int r = (int)(t / J.cols), c = (int)(t % J.cols);
       const float x = params[J.src + r * J.sr + c * J.sc];
-      const __nv_bfloat16 hi = __float2bfloat16_rn(x);
-      J.dst[(long long)r * J.ld + c] = hi;
-      if (J.lo_off) J.dst[J.lo_off + (long long)r * J.ld + c] = __float2bfloat16_rn(x - __bfloat162float(hi));
+      if constexpr (F16) {
+        reinterpret_cast<__half*>(J.dst)[(long long)r * J.ld + c] = __float2half_rn(x);
+      } else {
+        const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+        J.dst[(long long)r * J.ld + c] = hi;
+        if (J.lo_off) J.dst[J.lo_off + (long long)r * J.ld + c] = __float2bfloat16_rn(x - __bfloat162float(hi));
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------- FP32 -> BF16 (hi [+ lo])
+template <bool F16>
 __global__ void k_to_bf16(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, long long lo_off,
                           long long n8) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n8; t += (long long)gridDim.x * blockDim.x) {
@@ -32,9 +38,8 @@ __global__ void k_to_bf16(const float* __restrict__ in, __nv_bfloat16* __restric
     uint32_t hi[4], lo[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-      hi[i] = *reinterpret_cast<uint32_t*>(&h);
-      lo[i] = pack_bf16(v[2 * i] - __bfloat162float(h.x), v[2 * i + 1] - __bfloat162float(h.y));
+      if (lo_off) split2<false, true>(v[2 * i], v[2 * i + 1], hi[i], lo[i]);
+      else split2<F16, false>(v[2 * i], v[2 * i + 1], hi[i], lo[i]);
     }
     reinterpret_cast<uint4*>(out)[t] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
     if (lo_off) reinterpret_cast<uint4*>(out + lo_off)[t] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
@@ -45,7 +50,7 @@ __global__ void k_to_bf16(const float* __restrict__ in, __nv_bfloat16* __restric
 // a_i = sum_{k in [off_i, off_{i+1})} e'_k, FP32 accumulation in CSR order, one
 // warp per destination, lanes over 16-byte channel slices; output BF16 hi[+lo]
 // (the node GEMM operand and the layer checkpoint).  HBM-bound.
-template <int H>
+template <int H, bool F16>
 __global__ void __launch_bounds__(256) k_aggregate(const int* __restrict__ off, const float* __restrict__ e,
                                                    __nv_bfloat16* __restrict__ a, long long lo_off, int n) {
   constexpr int V = H / 4 / 32;  // float4 per lane
@@ -65,15 +70,16 @@ __global__ void __launch_bounds__(256) k_aggregate(const int* __restrict__ off, 
     }
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      __nv_bfloat162 h0 = __floats2bfloat162_rn(acc[v].x, acc[v].y);
-      __nv_bfloat162 h1 = __floats2bfloat162_rn(acc[v].z, acc[v].w);
-      uint2 hv = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
-      reinterpret_cast<uint2*>(a + (size_t)i * H)[lane + 32 * v] = hv;
+      uint32_t h0, h1, l0, l1;
       if (lo_off) {
-        uint2 lv = make_uint2(pack_bf16(acc[v].x - __bfloat162float(h0.x), acc[v].y - __bfloat162float(h0.y)),
-                              pack_bf16(acc[v].z - __bfloat162float(h1.x), acc[v].w - __bfloat162float(h1.y)));
-        reinterpret_cast<uint2*>(a + lo_off + (size_t)i * H)[lane + 32 * v] = lv;
+        split2<false, true>(acc[v].x, acc[v].y, h0, l0);
+        split2<false, true>(acc[v].z, acc[v].w, h1, l1);
+        reinterpret_cast<uint2*>(a + lo_off + (size_t)i * H)[lane + 32 * v] = make_uint2(l0, l1);
+      } else {
+        split2<F16, false>(acc[v].x, acc[v].y, h0, l0);
+        split2<F16, false>(acc[v].z, acc[v].w, h1, l1);
       }
+      reinterpret_cast<uint2*>(a + (size_t)i * H)[lane + 32 * v] = make_uint2(h0, h1);
     }
   }
 }
@@ -82,7 +88,7 @@ __global__ void __launch_bounds__(256) k_aggregate(const int* __restrict__ off, 
 // D[i][0:H]  = sum_{k in seg(i), rev_k < e_act} dZ1[rev_k]   (out-edges of i: d/dP_src)
 // D[i][H:2H] = sum_{k in seg(i), k < e_act}     dZ1[k]       (in-edges of i:  d/dP_dst)
 // dZ1 rows live as BF16 hi[+lo]; sums in FP32 in CSR order; output BF16 hi[+lo].
-template <int H>
+template <int H, bool F16>
 __global__ void __launch_bounds__(256) k_segsum(const int* __restrict__ off, const int* __restrict__ rev,
                                                 const __nv_bfloat16* __restrict__ dz, long long dz_lo,
                                                 __nv_bfloat16* __restrict__ D, long long d_lo, int n, int e_act) {
@@ -105,15 +111,14 @@ __global__ void __launch_bounds__(256) k_segsum(const int* __restrict__ off, con
         const int kk = srcpart ? rk : k;
         if (kk >= e_act) continue;
         const int c8 = srcpart ? ch : ch - H / 8;
-        uint4 u = reinterpret_cast<const uint4*>(dz + (size_t)kk * H)[c8];
-        const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+        float x[8];
+        unpack8<F16>(reinterpret_cast<const uint4*>(dz + (size_t)kk * H)[c8], x);
 #pragma unroll
-        for (int t = 0; t < 8; ++t) acc[v][t] += __bfloat162float(b[t]);
+        for (int t = 0; t < 8; ++t) acc[v][t] += x[t];
         if (dz_lo) {
-          uint4 w = reinterpret_cast<const uint4*>(dz + dz_lo + (size_t)kk * H)[c8];
-          const __nv_bfloat16* c = reinterpret_cast<const __nv_bfloat16*>(&w);
+          unpack8<false>(reinterpret_cast<const uint4*>(dz + dz_lo + (size_t)kk * H)[c8], x);
 #pragma unroll
-          for (int t = 0; t < 8; ++t) acc[v][t] += __bfloat162float(c[t]);
+          for (int t = 0; t < 8; ++t) acc[v][t] += x[t];
         }
       }
     }
@@ -123,9 +128,8 @@ __global__ void __launch_bounds__(256) k_segsum(const int* __restrict__ off, con
       uint32_t hi[4], lo[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(acc[v][2 * t], acc[v][2 * t + 1]);
-        hi[t] = *reinterpret_cast<uint32_t*>(&h);
-        lo[t] = pack_bf16(acc[v][2 * t] - __bfloat162float(h.x), acc[v][2 * t + 1] - __bfloat162float(h.y));
+        if (d_lo) split2<false, true>(acc[v][2 * t], acc[v][2 * t + 1], hi[t], lo[t]);
+        else split2<F16, false>(acc[v][2 * t], acc[v][2 * t + 1], hi[t], lo[t]);
       }
       reinterpret_cast<uint4*>(D + (size_t)i * 2 * H)[ch] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
       if (d_lo) reinterpret_cast<uint4*>(D + d_lo + (size_t)i * 2 * H)[ch] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(256) k_segsum(const int* __restrict__ off, con
 // copies exist.  gridDim = (Hin/128, Hout/NT, n_split); each CTA reduces a
 // fixed row range and writes its FP32 partial; k_reduce_part sums the splits
 // in order.
-template <int NT, bool SPLIT>
+template <int NT, bool SPLIT, bool F16>
 __global__ void __launch_bounds__(128, 1) k_wgrad(const __grid_constant__ WgradParams p) {
   constexpr int F = SPLIT ? 2 : 1;
   constexpr uint32_t A_HALF = 128 * 64 * 2, B_HALF = NT * 64 * 2;
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(128, 1) k_wgrad(const __grid_constant__ WgradP
       }
     }
   } else if (w == 1) {
-    constexpr uint32_t idesc = idesc_bf16(NT, true, true);
+    constexpr uint32_t idesc = idesc_bf16(NT, true, true, F16);
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % S;
       mbar_wait(&full[s], (kb / S) & 1);
@@ -266,55 +270,81 @@ __global__ void k_nonfinite(const float* __restrict__ x, long long n, int* __res
 }
 
 // ---------------------------------------------------------------- launchers
-void launch_pack(const float* params, const PackJob* jobs, int njobs, cudaStream_t st) {
-  k_pack<<<592, 256, 0, st>>>(params, jobs, njobs);
+void launch_pack(bool f16, const float* params, const PackJob* jobs, int njobs, cudaStream_t st) {
+  count_launch();
+  if (f16) k_pack<true><<<592, 256, 0, st>>>(params, jobs, njobs);
+  else k_pack<false><<<592, 256, 0, st>>>(params, jobs, njobs);
 }
-void launch_to_bf16(const float* in, __nv_bfloat16* out, long long lo_off, long long n, cudaStream_t st) {
+void launch_to_bf16(bool f16, const float* in, __nv_bfloat16* out, long long lo_off, long long n, cudaStream_t st) {
   if (n <= 0) return;
+  count_launch();
   long long n8 = n / 8;
   int blocks = (int)std::min<long long>((n8 + 255) / 256, 148 * 16);
-  k_to_bf16<<<blocks, 256, 0, st>>>(in, out, lo_off, n8);
+  if (f16) k_to_bf16<true><<<blocks, 256, 0, st>>>(in, out, lo_off, n8);
+  else k_to_bf16<false><<<blocks, 256, 0, st>>>(in, out, lo_off, n8);
 }
-void launch_aggregate(int H, const int* off, const float* e, __nv_bfloat16* a, long long lo_off, int n, cudaStream_t st) {
-  if (n <= 0) return;
+template <bool F16>
+static void agg_t(int H, const int* off, const float* e, __nv_bfloat16* a, long long lo_off, int n, cudaStream_t st) {
   int blocks = std::min((n + 7) / 8, 148 * 16);
-  if (H == 128) k_aggregate<128><<<blocks, 256, 0, st>>>(off, e, a, lo_off, n);
-  else if (H == 256) k_aggregate<256><<<blocks, 256, 0, st>>>(off, e, a, lo_off, n);
-  else k_aggregate<512><<<blocks, 256, 0, st>>>(off, e, a, lo_off, n);
+  if (H == 128) k_aggregate<128, F16><<<blocks, 256, 0, st>>>(off, e, a, lo_off, n);
+  else if (H == 256) k_aggregate<256, F16><<<blocks, 256, 0, st>>>(off, e, a, lo_off, n);
+  else k_aggregate<512, F16><<<blocks, 256, 0, st>>>(off, e, a, lo_off, n);
 }
-void launch_segsum(int H, const int* off, const int* rev, const __nv_bfloat16* dz, long long dz_lo, __nv_bfloat16* D,
-                   long long d_lo, int n, int e_act, cudaStream_t st) {
+void launch_aggregate(bool f16, int H, const int* off, const float* e, __nv_bfloat16* a, long long lo_off, int n,
+                      cudaStream_t st) {
   if (n <= 0) return;
+  count_launch();
+  if (f16) agg_t<true>(H, off, e, a, lo_off, n, st); else agg_t<false>(H, off, e, a, lo_off, n, st);
+}
+template <bool F16>
+static void seg_t(int H, const int* off, const int* rev, const __nv_bfloat16* dz, long long dz_lo, __nv_bfloat16* D,
+                  long long d_lo, int n, int e_act, cudaStream_t st) {
   int blocks = std::min((n + 7) / 8, 148 * 16);
-  if (H == 128) k_segsum<128><<<blocks, 256, 0, st>>>(off, rev, dz, dz_lo, D, d_lo, n, e_act);
-  else if (H == 256) k_segsum<256><<<blocks, 256, 0, st>>>(off, rev, dz, dz_lo, D, d_lo, n, e_act);
-  else k_segsum<512><<<blocks, 256, 0, st>>>(off, rev, dz, dz_lo, D, d_lo, n, e_act);
+  if (H == 128) k_segsum<128, F16><<<blocks, 256, 0, st>>>(off, rev, dz, dz_lo, D, d_lo, n, e_act);
+  else if (H == 256) k_segsum<256, F16><<<blocks, 256, 0, st>>>(off, rev, dz, dz_lo, D, d_lo, n, e_act);
+  else k_segsum<512, F16><<<blocks, 256, 0, st>>>(off, rev, dz, dz_lo, D, d_lo, n, e_act);
+}
+void launch_segsum(bool f16, int H, const int* off, const int* rev, const __nv_bfloat16* dz, long long dz_lo,
+                   __nv_bfloat16* D, long long d_lo, int n, int e_act, cudaStream_t st) {
+  if (n <= 0) return;
+  count_launch();
+  if (f16) seg_t<true>(H, off, rev, dz, dz_lo, D, d_lo, n, e_act, st);
+  else seg_t<false>(H, off, rev, dz, dz_lo, D, d_lo, n, e_act, st);
 }
 
-template <int NT, bool SPLIT>
+template <int NT, bool SPLIT, bool F16>
 static void wgrad_launch(const WgradParams& p, dim3 grid, cudaStream_t st) {
   constexpr int F = SPLIT ? 2 : 1;
   constexpr uint32_t STAGE = F * (128 * 64 * 2 + NT * 64 * 2);
   constexpr int S = (int)((220u * 1024u) / STAGE) > 6 ? 6 : (int)((220u * 1024u) / STAGE);
   size_t smem = 1024 + S * STAGE + 256;
-  auto kern = k_wgrad<NT, SPLIT>;
+  auto kern = k_wgrad<NT, SPLIT, F16>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, 128, smem, st>>>(p);
 }
-void launch_wgrad(const WgradParams& p, bool split, cudaStream_t st) {
+void launch_wgrad(const WgradParams& p, bool split, bool f16, cudaStream_t st) {
+  count_launch();
   const int NT = p.Hout >= 256 ? 256 : p.Hout;
   dim3 grid(p.Hin / 128, p.Hout / NT, p.n_split);
-  if (NT == 256) { if (split) wgrad_launch<256, true>(p, grid, st); else wgrad_launch<256, false>(p, grid, st); }
-  else { if (split) wgrad_launch<128, true>(p, grid, st); else wgrad_launch<128, false>(p, grid, st); }
+  if (NT == 256) {
+    if (f16) wgrad_launch<256, false, true>(p, grid, st); else wgrad_launch<256, false, false>(p, grid, st);
+  } else {
+    if (split) wgrad_launch<128, true, false>(p, grid, st);
+    else if (f16) wgrad_launch<128, false, true>(p, grid, st);
+    else wgrad_launch<128, false, false>(p, grid, st);
+  }
 }
 void launch_reduce_part(const float* part, int S, long long n, float* grad, cudaStream_t st) {
+  count_launch();
   int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
   k_reduce_part<<<blocks, 256, 0, st>>>(part, S, n, grad);
 }
 void launch_reduce_colsum(const float* part, int nblk, int nv, int H, ColsumDst d, float* grad, cudaStream_t st) {
+  count_launch();
   k_reduce_colsum<<<(nv * H + 255) / 256, 256, 0, st>>>(part, nblk, nv, H, d, grad);
 }
 void launch_nonfinite(const float* x, long long n, int* flag, cudaStream_t st) {
+  count_launch();
   k_nonfinite<<<592, 256, 0, st>>>(x, n, flag);
 }
 

@@ -13,18 +13,29 @@ struct ColsumDst {
   long long off[NV_MAX];  // destination offset of each column-sum vector in the gradient (-1 = unused)
 };
 
-void launch_pack(const float* params, const PackJob* jobs, int njobs, cudaStream_t st);
-void launch_to_bf16(const float* in, __nv_bfloat16* out, long long lo_off, long long n, cudaStream_t st);
-void launch_aggregate(int H, const int* off, const float* e, __nv_bfloat16* a, long long lo_off, int n,
+// `f16`: the 16-bit operand buffers hold FP16 instead of BF16 (XMGN_PREC_FP16).
+void launch_pack(bool f16, const float* params, const PackJob* jobs, int njobs, cudaStream_t st);
+void launch_to_bf16(bool f16, const float* in, __nv_bfloat16* out, long long lo_off, long long n, cudaStream_t st);
+void launch_aggregate(bool f16, int H, const int* off, const float* e, __nv_bfloat16* a, long long lo_off, int n,
                       cudaStream_t st);
-void launch_segsum(int H, const int* off, const int* rev, const __nv_bfloat16* dz, long long dz_lo,
+void launch_segsum(bool f16, int H, const int* off, const int* rev, const __nv_bfloat16* dz, long long dz_lo,
                    __nv_bfloat16* D, long long d_lo, int n, int e_act, cudaStream_t st);
-void launch_wgrad(const WgradParams& p, bool split, cudaStream_t st);
+void launch_wgrad(const WgradParams& p, bool split, bool f16, cudaStream_t st);
 void launch_reduce_part(const float* part, int S, long long n, float* grad, cudaStream_t st);
 void launch_reduce_colsum(const float* part, int nblk, int nv, int H, ColsumDst d, float* grad, cudaStream_t st);
 void launch_nonfinite(const float* x, long long n, int* flag, cudaStream_t st);
+// profiling (processor.cu): every kernel launch of the library is counted;
+// when enabled, named launch scopes are bracketed by CUDA events on their stream.
+void count_launch(int n = 1);
+struct ProfScope {
+  ProfScope(const char* name, cudaStream_t st);
+  ~ProfScope();
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr;
+};
 // chain.cu
-void launch_chain(int H, bool split, bool bwd, const ChainParams& p, int grid, cudaStream_t st);
+void launch_chain(int H, bool split, bool f16, bool bwd, const ChainParams& p, int grid, cudaStream_t st);
 size_t chain_smem(int H, bool split);
 
 }  // namespace xmgn

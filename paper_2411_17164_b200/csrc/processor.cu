@@ -38,7 +38,7 @@ struct xmgn_workspace {
   const xmgn_graph* g = nullptr;
   xmgn_model_cfg cfg{};
   int dev = 0, H = 0, L = 0, m = 0, sms = 148;
-  bool split = false;
+  bool split = false, f16 = false;
   int64_t Nmax = 0, Emax = 0, Rmax = 0;
   std::vector<xmgn::DPart> dparts;
   std::vector<void*> allocs;
@@ -170,7 +170,8 @@ static bool epi_writes_act(const Step& s) {
 }
 
 // Derive the ACT hand-off controls (chain.cuh) and launch.
-static void run_prog(xmgn_workspace* ws, Prog& pr, int M, const int* src, const int* dst, bool bwd, cudaStream_t st) {
+static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, const int* src, const int* dst, bool bwd,
+                     cudaStream_t st) {
   if (M <= 0) return;
   ChainParams& p = pr.p;
   p.n_steps = pr.n;
@@ -207,7 +208,8 @@ static void run_prog(xmgn_workspace* ws, Prog& pr, int M, const int* src, const 
   const int tiles = (M + 127) / 128;
   const int grid = tiles < ws->sms ? tiles : ws->sms;
   p.colsum = bwd ? ws->colsum : nullptr;
-  launch_chain(ws->H, ws->split, bwd, p, grid, st);
+  ProfScope ps(name, st);
+  launch_chain(ws->H, ws->split, ws->f16, bwd, p, grid, st);
   XMGN_CUDA(cudaGetLastError(), "chain kernel launch");
 }
 
@@ -246,7 +248,8 @@ static void wgrad(xmgn_workspace* ws, const BfBuf& a0, const BfBuf& a1, int a_wi
   if (S < 1) S = 1;
   p.n_split = S;
   p.part = ws->part;
-  launch_wgrad(p, ws->split, st);
+  ProfScope ps("wgrad", st);
+  launch_wgrad(p, ws->split, ws->f16, st);
   XMGN_CUDA(cudaGetLastError(), "wgrad launch");
   launch_reduce_part(ws->part, S, (long long)Hin * H, grad + dst, st);
 }
@@ -284,7 +287,8 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
     if (L < 1) return set_error(XMGN_EINVAL, "xmgn_workspace_create: layers=%d", L);
     if (cfg->precision == XMGN_PREC_FP32_CHECK && H != 128)
       return set_error(XMGN_EUNSUPPORTED, "xmgn_workspace_create: FP32 check mode is built for hidden=128 only");
-    if (cfg->precision != XMGN_PREC_BF16 && cfg->precision != XMGN_PREC_FP32_CHECK)
+    if (cfg->precision != XMGN_PREC_BF16 && cfg->precision != XMGN_PREC_FP32_CHECK &&
+        cfg->precision != XMGN_PREC_FP16)
       return set_error(XMGN_EINVAL, "xmgn_workspace_create: precision=%d", cfg->precision);
     if (L > g->depth)
       return set_error(XMGN_EHALO,
@@ -299,6 +303,7 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
       ws->dev = g->device;
       ws->H = H; ws->L = L; ws->m = m;
       ws->split = cfg->precision == XMGN_PREC_FP32_CHECK;
+      ws->f16 = cfg->precision == XMGN_PREC_FP16;
       cudaDeviceGetAttribute(&ws->sms, cudaDevAttrMultiProcessorCount, g->device);
       for (const Part& P : g->parts) {
         ws->Nmax = std::max(ws->Nmax, P.n_local);
@@ -381,10 +386,10 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
     const int H = ws->H, L = ws->L, m = ws->m;
     const long long NH = ws->Nmax * (long long)H, EH = ws->Emax * (long long)H;
     Layout Ly{H, L, m};
-    launch_pack(params, ws->d_jobs, ws->njobs, st);
+    launch_pack(ws->f16, params, ws->d_jobs, ws->njobs, st);
     const int64_t n0 = n_at(P, L, 0), e1 = e_at(P, L, 1);
-    launch_to_bf16(h0, ws->h_ck.p, ws->h_ck.lo, n0 * H, st);
-    launch_to_bf16(e0, ws->e_ck.p, ws->e_ck.lo, e1 * H, st);
+    launch_to_bf16(ws->f16, h0, ws->h_ck.p, ws->h_ck.lo, n0 * H, st);
+    launch_to_bf16(ws->f16, e0, ws->e_ck.p, ws->e_ck.lo, e1 * H, st);
     const int W1 = 0, W2 = 2;  // weight map slots
     auto r1 = [&](int l, int slot) { return (l * ws->S1 + slot) * H; };
     auto r2 = [&](int l, int slot) { return (l * ws->S2 + slot) * H; };
@@ -397,7 +402,7 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
         s.b_map = W1; s.b_row0 = r1(0, half ? SL_PDT : SL_PST);
         s.epi = EPI_STORE; s.f_out = ws->P; s.ld_out = 2 * H; s.col0 = half * H;
       }
-      run_prog(ws, pr, (int)n0, nullptr, nullptr, false, st);
+      run_prog(ws, "chain_proj", pr, (int)n0, nullptr, nullptr, false, st);
     }
     int cur = 0;
     for (int l = 1; l <= L; ++l) {
@@ -425,10 +430,11 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
         s.gamma = params + Ly.gamma(li, 0); s.beta = params + Ly.beta(li, 0);
         s.f_in = e_in; s.ld_in = H; s.f_out = e_out; s.ld_out = H;
         if (l < L) { s.flags |= EF_STORE_BF; s.bf_out = ws->e_ck.p + (long long)l * EH; s.bf_lo = ws->e_ck.lo; }
-        run_prog(ws, pr, (int)el, dp.src, dp.dst, false, st);
+        run_prog(ws, "chain_edge_fwd", pr, (int)el, dp.src, dp.dst, false, st);
       }
       // aggregation (Eq. 2) -> a^l (BF16 operand + checkpoint)
-      launch_aggregate(H, dp.off, e_out, ack.p, ack.lo, (int)nl, st);
+      { ProfScope ps("aggregate", st);
+      launch_aggregate(ws->f16, H, dp.off, e_out, ack.p, ack.lo, (int)nl, st); }
       XMGN_CUDA(cudaGetLastError(), "aggregate launch");
       {  // node update (Eq. 3) [+ P for layer l+1]
         Prog pr;
@@ -455,7 +461,7 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
             q.epi = EPI_STORE; q.f_out = ws->P; q.ld_out = 2 * H; q.col0 = half * H;
           }
         }
-        run_prog(ws, pr, (int)nl, nullptr, nullptr, false, st);
+        run_prog(ws, "chain_node_fwd", pr, (int)nl, nullptr, nullptr, false, st);
       }
       cur ^= 1;
     }
@@ -482,7 +488,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
     const int W1 = 0, W2 = 2;
     auto r1 = [&](int l, int slot) { return (l * ws->S1 + slot) * H; };
     auto r2 = [&](int l, int slot) { return (l * ws->S2 + slot) * H; };
-    launch_pack(params, ws->d_jobs, ws->njobs, st);
+    launch_pack(ws->f16, params, ws->d_jobs, ws->njobs, st);
     // seed: dL/dh^L on owned rows (the loss mask of PAPER.md:197 is the prefix)
     XMGN_CUDA(cudaMemcpyAsync(ws->Gh, grad_h_out, P.n_owned * H * sizeof(float), cudaMemcpyDeviceToDevice, st),
               "seed copy");
@@ -535,7 +541,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         Step& b = pr.add();   // da: G_a = dZ0 W0[agg rows]^T
         b.a_src = A_ACT; b.K = H; b.b_map = W1; b.b_row0 = r1(li, sl_n1a(m));
         b.epi = EPI_STORE; b.f_out = ws->Ga; b.ld_out = H; b.col0 = 0;
-        run_prog(ws, pr, (int)nl, nullptr, nullptr, true, st);
+        run_prog(ws, "chain_node_bwd", pr, (int)nl, nullptr, nullptr, true, st);
         colsum_reduce(ws, 1, li, grad_params, std::min(tiles_n, ws->sms), st);
         wgrad(ws, hck, ack, H, H / 128, ws->scrZ[0], H, 0, nl, 2 * H, grad_params, Ly.W(li, 1, 0), st);
         for (int j = 1; j <= m; ++j)
@@ -550,7 +556,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
           s.b_map = W1; s.b_row0 = r1(li, half ? SL_PDT : SL_PST);
           s.epi = EPI_STORE; s.f_out = ws->P; s.ld_out = 2 * H; s.col0 = half * H;
         }
-        run_prog(ws, pr, (int)nprev, nullptr, nullptr, false, st);
+        run_prog(ws, "chain_proj", pr, (int)nprev, nullptr, nullptr, false, st);
       }
       {  // edge block backward
         Prog pr;
@@ -560,14 +566,15 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         a.a_src = A_ACT; a.K = H; a.b_map = W1; a.b_row0 = r1(li, sl_e1e(m));
         a.epi = EPI_ADD; a.f_in = ws->Ge; a.f_out = ws->Ge; a.ld_in = a.ld_out = H; a.valid_in = (int)enext;
         a.flags = EF_GATHER_G; a.gather = ws->Ga;
-        run_prog(ws, pr, (int)el, dp.src, dp.dst, true, st);
+        run_prog(ws, "chain_edge_bwd", pr, (int)el, dp.src, dp.dst, true, st);
         colsum_reduce(ws, 0, li, grad_params, std::min(tiles_e, ws->sms), st);
         wgrad(ws, eck, none, H, H / 128, ws->scrZ[0], H, 0, el, H, grad_params, Ly.W(li, 0, 0), st);
         for (int j = 1; j <= m; ++j)
           wgrad(ws, ws->scrA[j - 1], none, H, H / 128, ws->scrZ[j], H, 0, el, H, grad_params, Ly.W(li, 0, j), st);
       }
       // D = [sum over out-edges | sum over in-edges] of dZ0 (adjoint of the P gathers)
-      launch_segsum(H, dp.off, dp.rev, ws->scrZ[0].p, ws->scrZ[0].lo, ws->D.p, ws->D.lo, (int)nprev, (int)el, st);
+      { ProfScope ps("segsum", st);
+      launch_segsum(ws->f16, H, dp.off, dp.rev, ws->scrZ[0].p, ws->scrZ[0].lo, ws->D.p, ws->D.lo, (int)nprev, (int)el, st); }
       XMGN_CUDA(cudaGetLastError(), "segsum launch");
       {  // G_h^{l-1} = [rows < n_l] G_h + D [W_s | W_d]^T
         Prog pr;
@@ -575,7 +582,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         Step& s = pr.add();
         s.a_src = A_TMA; s.a_map0 = 4; s.K = 2 * H; s.b_map = W2; s.b_row0 = r2(li, SL2_SD);
         s.epi = EPI_ADD; s.f_in = ws->Gh; s.f_out = ws->Gh; s.ld_in = s.ld_out = H; s.valid_in = (int)nl;
-        run_prog(ws, pr, (int)nprev, nullptr, nullptr, false, st);
+        run_prog(ws, "chain_projbwd", pr, (int)nprev, nullptr, nullptr, false, st);
       }
       // dW_s = h^T D_src, dW_d = h^T D_dst
       wgrad(ws, hck, none, H, H / 128, ws->D, 2 * H, 0, nprev, H, grad_params, Ly.W(li, 0, 0) + (long long)H * H, st);

@@ -12,6 +12,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 namespace xmgn {
 
@@ -92,11 +93,11 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo, ui
   d |= (uint64_t)2 << 61;   // SWIZZLE_128B
   return d;
 }
-// Instruction descriptor, kind::f16: BF16 x BF16 -> FP32, M=128, N, majors.
-__host__ __device__ constexpr uint32_t idesc_bf16(int N, bool a_mn_major, bool b_mn_major) {
+// Instruction descriptor, kind::f16: (BF16|FP16) x same -> FP32, M=128, N, majors.
+__host__ __device__ constexpr uint32_t idesc_bf16(int N, bool a_mn_major, bool b_mn_major, bool f16 = false) {
   return (1u << 4)                  // D = F32
-         | (1u << 7)                // A = BF16
-         | (1u << 10)               // B = BF16
+         | ((f16 ? 0u : 1u) << 7)   // A = BF16 (1) or FP16 (0)
+         | ((f16 ? 0u : 1u) << 10)  // B = BF16 (1) or FP16 (0)
          | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16)
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
@@ -154,6 +155,41 @@ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t chunk) {
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&t);
+}
+
+// 16-bit operand format of the fast paths: BF16 (paper's AMP format) or FP16.
+// split2: hi = round(a,b); lo = round(residual) (only used with BF16 SPLIT).
+template <bool F16>
+__device__ __forceinline__ uint32_t pack16(float a, float b) {
+  if constexpr (F16) {
+    __half2 t = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&t);
+  } else {
+    return pack_bf16(a, b);
+  }
+}
+template <bool F16, bool SPLIT>
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  if constexpr (SPLIT) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    hi = *reinterpret_cast<uint32_t*>(&h);
+    lo = pack_bf16(a - __bfloat162float(h.x), b - __bfloat162float(h.y));
+  } else {
+    hi = pack16<F16>(a, b);
+    lo = 0;
+  }
+}
+template <bool F16>
+__device__ __forceinline__ void unpack8(const uint4& u, float* v) {
+  if constexpr (F16) {
+    const __half* h = reinterpret_cast<const __half*>(&u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __half2float(h[i]);
+  } else {
+    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __bfloat162float(h[i]);
+  }
 }
 
 }  // namespace xmgn

@@ -16,7 +16,7 @@ if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
 _lib = ctypes.CDLL(LIB_PATH)
 
-PREC_BF16, PREC_FP32_CHECK = 0, 1
+PREC_BF16, PREC_FP32_CHECK, PREC_FP16 = 0, 1, 2
 STATUS = {0: "OK", 1: "EINVAL", 2: "EHALO", 3: "ESTATE", 4: "ENOMEM", 5: "ECUDA", 6: "ENCCL",
           7: "ENONFINITE", 8: "EUNSUPPORTED"}
 
@@ -70,12 +70,16 @@ _sig("xmgn_comm_init", _i32, [ctypes.c_char_p, _i32, _i32, _i32, ctypes.POINTER(
 _sig("xmgn_grad_reduce", _i32, [_vp, _vp, _sz, _vp])
 _sig("xmgn_comm_destroy", None, [_vp])
 _sig("xmgn_selftest_gemm", _i32, [_i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp])
+_sig("xmgn_launch_count", ctypes.c_longlong, [])
+_sig("xmgn_profile_enable", _i32, [_i32])
+_sig("xmgn_profile_collect", _i32, [ctypes.c_char_p, _sz, ctypes.POINTER(ctypes.c_double),
+                                    ctypes.POINTER(ctypes.c_longlong), _i32, ctypes.POINTER(_i32)])
 
 EXPORTS = ["xmgn_last_error", "xmgn_version", "xmgn_load_graph", "xmgn_part_info_get", "xmgn_export_part",
            "xmgn_free_graph", "xmgn_param_count", "xmgn_workspace_create", "xmgn_workspace_bytes",
            "xmgn_workspace_free", "xmgn_processor_fwd", "xmgn_processor_bwd", "xmgn_check_finite",
            "xmgn_comm_unique_id", "xmgn_comm_init", "xmgn_grad_reduce", "xmgn_comm_destroy",
-           "xmgn_selftest_gemm"]
+           "xmgn_selftest_gemm", "xmgn_launch_count", "xmgn_profile_enable", "xmgn_profile_collect"]
 
 
 def _check(status):
@@ -146,9 +150,9 @@ class Graph:
         return out
 
     def close(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and _lib is not None:
             _lib.xmgn_free_graph(self.handle)
-            self.handle = None
+        self.handle = None
 
     def __del__(self):
         self.close()
@@ -183,9 +187,9 @@ class Workspace:
                                        _ptr(grad_params), _ptr(grad_h0), _ptr(grad_e0), _stream(stream)))
 
     def close(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and _lib is not None:
             _lib.xmgn_workspace_free(self.handle)
-            self.handle = None
+        self.handle = None
 
     def __del__(self):
         self.close()
@@ -216,6 +220,25 @@ class Comm:
         if getattr(self, "handle", None):
             _lib.xmgn_comm_destroy(self.handle)
             self.handle = None
+
+
+def launch_count():
+    return int(_lib.xmgn_launch_count())
+
+
+def profile_enable(on=True):
+    _check(_lib.xmgn_profile_enable(int(on)))
+
+
+def profile_collect():
+    """{scope name: (total ms, launches)} since the last collect."""
+    buf = ctypes.create_string_buffer(4096)
+    ms = (ctypes.c_double * 64)()
+    cnt = (ctypes.c_longlong * 64)()
+    n = _i32()
+    _check(_lib.xmgn_profile_collect(buf, 4096, ms, cnt, 64, ctypes.byref(n)))
+    names = buf.value.decode().split("\n")
+    return {names[i]: (ms[i], int(cnt[i])) for i in range(n.value)}
 
 
 def selftest_gemm(A, B, C, a_mn_major, b_mn_major, M, N, K, stream=None):

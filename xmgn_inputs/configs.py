@@ -22,7 +22,9 @@ CONFIGS = {
     "cfg5": dict(shape="car", levels=[2_500_000, 5_000_000, 10_000_000], k=6, H=512, L=15, P=32, prec="bf16"),
 }
 
-CACHE = os.environ.get("XMGN_CACHE", os.path.join(os.path.dirname(os.path.dirname(__file__)), "data", "cache"))
+# Outside the repo so it never travels with a gpurun snapshot; only a cache
+# (missing entries are regenerated deterministically).
+CACHE = os.environ.get("XMGN_CACHE", os.path.join(os.path.expanduser("~"), ".cache", "xmgn_graphs"))
 
 
 def build(shape, levels, k, P, halo, seed=0):
