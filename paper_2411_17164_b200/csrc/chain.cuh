@@ -43,7 +43,10 @@ enum : int {
   EF_STORE_S = 4,      // EPI_SILU: scratch S = SiLU'(v)
   EF_WRITE_ACT = 8,    // EPI_LN_FWD: also write the BF16 output into ACT
   EF_GATHER_G = 16,    // EPI_LN_BWD / EPI_ADD: add Ga[dst][c]
-  EF_STORE_BF = 32     // EPI_LN_FWD: write bf16 output (checkpoint)
+  EF_STORE_BF = 32,    // EPI_LN_FWD: write bf16 output (checkpoint)
+  EF_RES16 = 64,       // EPI_LN_FWD: residual input is the 16-bit tensor res16 (else fp32 f_in)
+  EF_STORE_F32 = 128,  // EPI_LN_FWD: write the fp32 output f_out
+  EF_OUT16 = 256       // EPI_STORE: write 16-bit bf_out (ld_out, col0) instead of fp32 f_out
 };
 
 enum : int {
@@ -70,11 +73,19 @@ struct Step {
   __nv_bfloat16* scr_z;      // scratch dZ
   long long lo_off;          // element offset of the lo half of the scratch buffers (SPLIT)
   long long bf_lo;           // element offset of the lo half of bf_out (SPLIT)
+  const __nv_bfloat16* res16;  // 16-bit residual rows [rows][H] (EF_RES16); lo at res16 + res16_lo
+  long long res16_lo;
+  const __nv_bfloat16* gather16;  // 16-bit P [N][2H] (EF_GATHER_P); lo at + gather16_lo
+  long long gather16_lo;
 };
 
 constexpr int MAX_STEPS = 8;
 constexpr int MAX_MAPS = 8;
 constexpr int NV_MAX = 5;  // column-sum vectors per kernel
+// Epilogue: EPI_GROUPS warps per TMEM lane quadrant, each owning H/EPI_GROUPS
+// columns of its 32 rows (row statistics are exchanged through shared memory).
+constexpr int EPI_GROUPS = 2;
+constexpr int CHAIN_THREADS = 128 + 128 * EPI_GROUPS;
 
 struct ChainParams {
   CUtensorMap maps[MAX_MAPS];
@@ -90,21 +101,24 @@ struct ChainParams {
 template <int H, bool SPLIT>
 struct ChainCfg {
   static constexpr int F = SPLIT ? 2 : 1;
-  static constexpr int NB = H < 256 ? H : 256;                 // N rows per B slot / MMA
+  static constexpr int NB = H < 256 ? H : 256;                 // MMA N (columns per N-half)
+  static constexpr int NBH = NB / 2;                           // B rows held by each CTA of the pair
   static constexpr uint32_t ACT_HALF = 128u * H * 2u;          // one BF16 copy of the ACT tile
   static constexpr uint32_t ACT_BYTES = F * ACT_HALF;
   static constexpr uint32_t A_SLOT_HALF = 128u * 64u * 2u;     // 16 KiB
   static constexpr uint32_t A_SLOT = F * A_SLOT_HALF;
   static constexpr int SA = ACT_BYTES / A_SLOT;
-  static constexpr uint32_t B_SLOT_HALF = NB * 128u;
+  static constexpr uint32_t B_SLOT_HALF = NBH * 128u;
   static constexpr uint32_t B_SLOT = F * B_SLOT_HALF;
   static constexpr uint32_t SMEM_LIMIT = 227u * 1024u;
-  static constexpr int SB_FIT = (int)((SMEM_LIMIT - 2048u - ACT_BYTES) / B_SLOT);
+  static constexpr int SB_FIT = (int)((SMEM_LIMIT - 2560u - ACT_BYTES) / B_SLOT);
   static constexpr int SB = SB_FIT > 8 ? 8 : SB_FIT;
   static constexpr uint32_t BAR_OFF = ACT_BYTES + SB * B_SLOT;
-  static constexpr uint32_t SMEM_BYTES = BAR_OFF + 512 + 1024;  // + barriers + alignment slack
+  static constexpr uint32_t RED_OFF = BAR_OFF + 512;             // row-reduction exchange [EW][128] f32
+  static constexpr uint32_t SMEM_BYTES = RED_OFF + EPI_GROUPS * 128 * 4 + 1024;  // + alignment slack
   static constexpr uint32_t TMEM_COLS = H;
   static_assert(SB >= 2, "B ring too small");
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
 __device__ __forceinline__ float sigmoid_fast(float v) {
@@ -116,6 +130,25 @@ template <bool ACCURATE>
 __device__ __forceinline__ float sigmoid_(float v) {
   if constexpr (ACCURATE) return 1.0f / (1.0f + __expf(-v));
   else return sigmoid_fast(v);
+}
+// SiLU(x) = x*sigmoid(x) = h + h*tanh(h), h = x/2 (one MUFU op on the fast path)
+template <bool ACCURATE>
+__device__ __forceinline__ float silu_(float x) {
+  if constexpr (ACCURATE) {
+    return x / (1.0f + __expf(-x));
+  } else {
+    const float h = 0.5f * x;
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+    return fmaf(h, t, h);
+  }
+}
+// SiLU and SiLU' = s (1 + x (1 - s)), s = sigmoid(x)
+template <bool ACCURATE>
+__device__ __forceinline__ void silu_and_grad(float x, float& y, float& dy) {
+  const float sg = sigmoid_<ACCURATE>(x);
+  y = x * sg;
+  dy = sg * fmaf(x, 1.0f - sg, 1.0f);
 }
 
 // Store 32 consecutive values (cols c0..c0+31) of row `row` into a swizzled
@@ -129,9 +162,13 @@ __device__ __forceinline__ void store_tile32(uint8_t* tile, uint32_t lo_off, int
     uint32_t hi[4], lo[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) split2<F16, SPLIT>(v[q * 8 + 2 * i], v[q * 8 + 2 * i + 1], hi[i], lo[i]);
-    uint32_t off = sw128_off(row, q0 + q);
-    *reinterpret_cast<uint4*>(blk + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    if constexpr (SPLIT) *reinterpret_cast<uint4*>(blk + lo_off + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    const uint32_t a = smem_u32(blk) + sw128_off(row, q0 + q);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3])
+                 : "memory");
+    if constexpr (SPLIT)
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a + lo_off), "r"(lo[0]), "r"(lo[1]), "r"(lo[2]),
+                   "r"(lo[3])
+                   : "memory");
   }
 }
 
@@ -169,6 +206,13 @@ __device__ __forceinline__ void load_f32x32(const float* p, float* v) {
     v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
   }
 }
+__device__ __forceinline__ void load_f32x32_ro(const float* p, float* v) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float4 t = __ldg(reinterpret_cast<const float4*>(p) + q);
+    v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+  }
+}
 __device__ __forceinline__ void store_f32x32(float* p, const float* v) {
 #pragma unroll
   for (int q = 0; q < 8; ++q)
@@ -192,12 +236,32 @@ __device__ __forceinline__ float warp_colsum32(float* v) {
   return v[0];
 }
 
+// dY of the LayerNorm backward: incoming gradient rows (< valid_in) plus the
+// aggregation adjoint G_a[dst] for edge programs.
+__device__ __forceinline__ void load_dy(const Step& st, bool has_g, bool valid, int r, int dst, int c0, float* dy) {
+  if (has_g) load_f32x32(st.f_in + (size_t)r * st.ld_in + c0, dy);
+  else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) dy[i] = 0.f;
+  }
+  if (valid && (st.flags & EF_GATHER_G)) {
+    float ga[32];
+    load_f32x32(st.gather + (size_t)dst * st.ld_in + c0, ga);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) dy[i] += ga[i];
+  }
+}
+
 template <int H, bool SPLIT, bool BWD, bool F16>
-__global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainParams p) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
+    k_chain(const __grid_constant__ ChainParams p) {
   using C = ChainCfg<H, SPLIT>;
-  constexpr int F = C::F;
   constexpr int NB = C::NB;
-  constexpr int NH = H / NB;      // N-halves per step
+  constexpr int NH = H / NB;           // N-halves per step
+  constexpr int EW = EPI_GROUPS;
+  constexpr int HC = H / EW;           // columns per epilogue warp
+  constexpr int NC = HC / 32;          // 32-column chunks per epilogue warp
+  constexpr int NEPI = 128 * EW;       // epilogue threads
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* act = smem;                       // ACT tile (and A ring)
@@ -213,58 +277,65 @@ __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainP
   uint64_t* act_free = act_full + 1;         // MMA -> producer (no MMA reads ACT any more)
   uint64_t* mma_idle = act_free + 1;         // MMA -> itself (all issued MMAs retired)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(mma_idle + 1);
+  float* red = reinterpret_cast<float*>(smem + C::RED_OFF);
 
   const int w = warp_id();
-  const int n_tiles = (p.M + 127) / 128;
+  const uint32_t rank = cluster_ctarank();
+  const int cid = (int)cluster_id_x(), ncl = (int)n_clusters_x();
+  const int n_tiles = (p.M + 255) / 256;     // pair tiles of 256 rows (128 per CTA)
+  constexpr int EPI_WARPS = NEPI / 32;
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::SA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < C::SB; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
     mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 128);
-    mbar_init(act_full, 128);
+    mbar_init(acc_empty, 2 * EPI_WARPS);   // one arrival per epilogue warp of both CTAs
+    mbar_init(act_full, 2 * EPI_WARPS);
     mbar_init(act_free, 1);
     mbar_init(mma_idle, 1);
     fence_barrier_init();
   }
   if (w == 0 && lane_id() == 0)
     for (int i = 0; i < MAX_MAPS; ++i) tma_prefetch(&p.maps[i]);
-  if (w == 2) tmem_alloc(tslot, C::TMEM_COLS);
+  if (w == 2) tmem_alloc_cg2(tslot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
   if (w == 0) {
-    // ============================ TMA producer
+    // ============================ TMA producer (both CTAs: own A rows, own half of B)
     if (elect_one()) {
       int ai = 0, bi = 0, g = 0, naf = 0;  // A / B ring fills, global step, act_free phases
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int row0 = tile * 128;
+      for (int tile = cid; tile < n_tiles; tile += ncl) {
+        const int row0 = tile * 256 + (int)rank * 128;
         for (int s = 0; s < p.n_steps; ++s, ++g) {
           const Step& st = p.steps[s];
           const bool tma_a = st.a_src == A_TMA;
-          if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) { mbar_wait(act_free, naf & 1); ++naf; }
+          if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) { mbar_wait_cluster(act_free, naf & 1); ++naf; }
           for (int kc = 0; kc < st.K / 64; ++kc) {
             if (tma_a) {
               const int slot = ai % C::SA;
-              if (ai >= C::SA) mbar_wait(&a_empty[slot], ((ai / C::SA) - 1) & 1);
-              mbar_expect_tx(&a_full[slot], C::A_SLOT);
+              if (ai >= C::SA) mbar_wait_cluster(&a_empty[slot], ((ai / C::SA) - 1) & 1);
+              if (rank == 0) mbar_expect_tx(&a_full[slot], 2 * C::A_SLOT);
+              const uint32_t fb = mapa_shared(smem_u32(&a_full[slot]), 0);
               uint8_t* dstp = act + slot * C::A_SLOT;
               const int k = kc * 64;
               const int mi = (st.a_map1 >= 0 && k >= st.a_ksplit) ? st.a_map1 : st.a_map0;
               const int kk = (st.a_map1 >= 0 && k >= st.a_ksplit) ? k - st.a_ksplit : k;
-              tma_load_2d(dstp, &p.maps[mi], &a_full[slot], kk, row0);
-              if constexpr (SPLIT) tma_load_2d(dstp + C::A_SLOT_HALF, &p.maps[mi + 1], &a_full[slot], kk, row0);
+              tma_load_2d_cg2(dstp, &p.maps[mi], fb, kk, row0);
+              if constexpr (SPLIT) tma_load_2d_cg2(dstp + C::A_SLOT_HALF, &p.maps[mi + 1], fb, kk, row0);
               ++ai;
             }
             for (int nh = 0; nh < NH; ++nh) {
               const int slot = bi % C::SB;
-              if (bi >= C::SB) mbar_wait(&b_empty[slot], ((bi / C::SB) - 1) & 1);
-              mbar_expect_tx(&b_full[slot], C::B_SLOT);
+              if (bi >= C::SB) mbar_wait_cluster(&b_empty[slot], ((bi / C::SB) - 1) & 1);
+              if (rank == 0) mbar_expect_tx(&b_full[slot], 2 * C::B_SLOT);
+              const uint32_t fb = mapa_shared(smem_u32(&b_full[slot]), 0);
               uint8_t* dstp = bring + slot * C::B_SLOT;
-              tma_load_2d(dstp, &p.maps[st.b_map], &b_full[slot], kc * 64, st.b_row0 + nh * NB);
-              if constexpr (SPLIT)
-                tma_load_2d(dstp + C::B_SLOT_HALF, &p.maps[st.b_map + 1], &b_full[slot], kc * 64, st.b_row0 + nh * NB);
+              const int brow = st.b_row0 + nh * NB + (int)rank * C::NBH;
+              tma_load_2d_cg2(dstp, &p.maps[st.b_map], fb, kc * 64, brow);
+              if constexpr (SPLIT) tma_load_2d_cg2(dstp + C::B_SLOT_HALF, &p.maps[st.b_map + 1], fb, kc * 64, brow);
               ++bi;
             }
           }
@@ -272,88 +343,109 @@ __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainP
       }
     }
   } else if (w == 1) {
-    // ============================ MMA issuer
-    constexpr uint32_t idesc = idesc_bf16(NB, false, false, F16);
-    int ai = 0, bi = 0, g = 0, nact = 0, nidle = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      for (int s = 0; s < p.n_steps; ++s, ++g) {
-        const Step& st = p.steps[s];
-        const bool tma_a = st.a_src == A_TMA;
-        if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) {
-          // let every issued MMA (the ones reading ACT) retire, then hand ACT
-          // to the producer as A-ring space; the pending epilogue overlaps.
-          if (elect_one()) mma_commit(mma_idle);
-          __syncwarp();
-          mbar_wait(mma_idle, nidle & 1);
-          ++nidle;
-          if (elect_one()) mbar_arrive(act_free);
-          __syncwarp();
-        }
-        if (g > 0) mbar_wait(acc_empty, (g - 1) & 1);
-        if (st.ctl & CTL_WAIT_ACT) { mbar_wait(act_full, nact & 1); ++nact; }
-        tc_fence_after();
-        for (int kc = 0; kc < st.K / 64; ++kc) {
-          int aslot = 0;
-          uint32_t a_base;
-          if (tma_a) {
-            aslot = ai % C::SA;
-            mbar_wait(&a_full[aslot], (ai / C::SA) & 1);
-            a_base = smem_u32(act + aslot * C::A_SLOT);
-          } else {
-            a_base = smem_u32(act + kc * (128 * 128));
+    // ============================ MMA issuer (leader CTA only; M = 256 pair MMAs)
+    if (rank == 0) {
+      constexpr uint32_t idesc = idesc_pair(NB, F16);
+      const uint32_t act_free_peer = mapa_shared(smem_u32(act_free), 1);
+      int ai = 0, bi = 0, g = 0, nact = 0, nidle = 0;
+      for (int tile = cid; tile < n_tiles; tile += ncl) {
+        for (int s = 0; s < p.n_steps; ++s, ++g) {
+          const Step& st = p.steps[s];
+          const bool tma_a = st.a_src == A_TMA;
+          if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) {
+            // let every issued MMA (the ones reading ACT) retire, then hand both
+            // CTAs' ACT tiles to their producers as A-ring space.
+            if (elect_one()) mma_commit_cg2_mc(mma_idle, 1);
+            __syncwarp();
+            mbar_wait(mma_idle, nidle & 1);
+            ++nidle;
+            if (elect_one()) { mbar_arrive(act_free); mbar_arrive_cluster(act_free_peer); }
+            __syncwarp();
           }
-          const uint32_t a_lo = tma_a ? C::A_SLOT_HALF : C::ACT_HALF;
-          for (int nh = 0; nh < NH; ++nh) {
-            const int bslot = bi % C::SB;
-            mbar_wait(&b_full[bslot], (bi / C::SB) & 1);
-            tc_fence_after();
-            const uint32_t b_base = smem_u32(bring + bslot * C::B_SLOT);
-            if (elect_one()) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const uint32_t acc = (kc | k) != 0;
-                const uint32_t d = tmem + nh * NB;
-                uint64_t ad = sdesc_sw128(a_base + k * 32, 16, 1024);
-                uint64_t bd = sdesc_sw128(b_base + k * 32, 16, 1024);
-                mma_bf16(d, ad, bd, idesc, acc);
-                if constexpr (SPLIT) {
-                  uint64_t adl = sdesc_sw128(a_base + a_lo + k * 32, 16, 1024);
-                  uint64_t bdl = sdesc_sw128(b_base + C::B_SLOT_HALF + k * 32, 16, 1024);
-                  mma_bf16(d, adl, bd, idesc, 1);
-                  mma_bf16(d, ad, bdl, idesc, 1);
-                }
-              }
-              mma_commit(&b_empty[bslot]);
+          if (g > 0) mbar_wait_cluster(acc_empty, (g - 1) & 1);
+          if (st.ctl & CTL_WAIT_ACT) { mbar_wait_cluster(act_full, nact & 1); ++nact; }
+          tc_fence_after();
+          for (int kc = 0; kc < st.K / 64; ++kc) {
+            int aslot = 0;
+            uint32_t a_base;
+            if (tma_a) {
+              aslot = ai % C::SA;
+              mbar_wait_cluster(&a_full[aslot], (ai / C::SA) & 1);
+              a_base = smem_u32(act + aslot * C::A_SLOT);
+            } else {
+              a_base = smem_u32(act + kc * (128 * 128));
             }
-            __syncwarp();
-            ++bi;
+            const uint32_t a_lo = tma_a ? C::A_SLOT_HALF : C::ACT_HALF;
+            for (int nh = 0; nh < NH; ++nh) {
+              const int bslot = bi % C::SB;
+              mbar_wait_cluster(&b_full[bslot], (bi / C::SB) & 1);
+              tc_fence_after();
+              const uint32_t b_base = smem_u32(bring + bslot * C::B_SLOT);
+              if (elect_one()) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const uint32_t acc = (kc | k) != 0;
+                  const uint32_t d = tmem + nh * NB;
+                  uint64_t ad = sdesc_sw128(a_base + k * 32, 16, 1024);
+                  uint64_t bd = sdesc_sw128(b_base + k * 32, 16, 1024);
+                  mma_f16_cg2(d, ad, bd, idesc, acc);
+                  if constexpr (SPLIT) {
+                    uint64_t adl = sdesc_sw128(a_base + a_lo + k * 32, 16, 1024);
+                    uint64_t bdl = sdesc_sw128(b_base + C::B_SLOT_HALF + k * 32, 16, 1024);
+                    mma_f16_cg2(d, adl, bd, idesc, 1);
+                    mma_f16_cg2(d, ad, bdl, idesc, 1);
+                  }
+                }
+                mma_commit_cg2_mc(&b_empty[bslot], 3);
+              }
+              __syncwarp();
+              ++bi;
+            }
+            if (tma_a) {
+              if (elect_one()) mma_commit_cg2_mc(&a_empty[aslot], 3);
+              __syncwarp();
+              ++ai;
+            }
           }
-          if (tma_a) {
-            if (elect_one()) mma_commit(&a_empty[aslot]);
-            __syncwarp();
-            ++ai;
-          }
+          if (elect_one()) mma_commit_cg2_mc(acc_full, 3);
+          __syncwarp();
         }
-        if (elect_one()) mma_commit(acc_full);
-        __syncwarp();
       }
     }
   } else if (w >= 4) {
-    // ============================ epilogue (thread = tile row = TMEM lane)
-    const int q = w & 3;
+    // ============================ epilogue: thread = tile row (TMEM lane) x HC columns
+    const int q = w & 3;                 // TMEM lane quadrant
+    const int eg = (w - 4) >> 2;         // column group
     const int lane = lane_id();
     const int trow = q * 32 + lane;
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    float colacc[BWD ? NV_MAX : 1][BWD ? H / 32 : 1];
+    const int cb = eg * HC;              // first column of this thread
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + cb;
+    // full-row sum of a per-thread partial, identical bits in every group
+    auto row_sum = [&](float x) -> float {
+      if constexpr (EW == 1) {
+        return x;
+      } else {
+        red[eg * 128 + trow] = x;
+        named_bar(1 + q, 32 * EW);
+        float t = red[trow];
+#pragma unroll
+        for (int j = 1; j < EW; ++j) t += red[j * 128 + trow];
+        named_bar(1 + q, 32 * EW);
+        return t;
+      }
+    };
+    float colacc[BWD ? NV_MAX : 1][BWD ? NC : 1];
     if constexpr (BWD) {
 #pragma unroll
       for (int a = 0; a < NV_MAX; ++a)
 #pragma unroll
-        for (int b = 0; b < H / 32; ++b) colacc[a][b] = 0.f;
+        for (int b = 0; b < NC; ++b) colacc[a][b] = 0.f;
     }
+    const uint32_t acc_empty_l = mapa_shared(smem_u32(acc_empty), 0);
+    const uint32_t act_full_l = mapa_shared(smem_u32(act_full), 0);
     int g = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const int r = tile * 128 + trow;
+    for (int tile = cid; tile < n_tiles; tile += ncl) {
+      const int r = tile * 256 + (int)rank * 128 + trow;
       const bool valid = r < p.M;
       const int rr = valid ? r : 0;
       const int src = p.src ? p.src[rr] : 0;
@@ -363,65 +455,81 @@ __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainP
         mbar_wait(acc_full, g & 1);
         tc_fence_after();
         bool wrote_act = false;
-        float v[32];
+        float v[32], pb[32];
         if (st.epi == EPI_SILU) {
 #pragma unroll 1
-          for (int c0 = 0; c0 < H; c0 += 32) {
-            tmem_ld32(tl + c0, v);
-            float g1[32], g2[32];
+          for (int cc = 0; cc < NC; ++cc) {
+            const int c0 = cb + cc * 32;
+            tmem_ld32(tl + cc * 32, v);
+            load_f32x32_ro(st.bias + c0, pb);
             if (st.flags & EF_GATHER_P) {
-              load_f32x32(st.gather + (size_t)src * 2 * H + c0, g1);
-              load_f32x32(st.gather + (size_t)dst * 2 * H + H + c0, g2);
-            }
-            float sv[32], dv[32];
+              float g1[32];
+              load_bf32<SPLIT, F16>(st.gather16 + (size_t)src * 2 * H + c0, st.gather16_lo, g1);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              float x = v[i] + __ldg(st.bias + c0 + i);
-              if (st.flags & EF_GATHER_P) x += g1[i] + g2[i];
-              float sg = sigmoid_<SPLIT>(x);
-              sv[i] = x * sg;
-              dv[i] = sg * (1.0f + x * (1.0f - sg));
+              for (int i = 0; i < 32; ++i) pb[i] += g1[i];
+              load_bf32<SPLIT, F16>(st.gather16 + (size_t)dst * 2 * H + H + c0, st.gather16_lo, g1);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) pb[i] += g1[i];
+            }
+            float sv[32];
+            if (st.flags & EF_STORE_S) {
+              float dv[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float x = v[i] + pb[i];
+                silu_and_grad<SPLIT>(x, sv[i], dv[i]);
+              }
+              if (valid) store_bf32<SPLIT, F16>(st.scr_s + (size_t)r * H + c0, st.lo_off, dv);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) sv[i] = silu_<SPLIT>(v[i] + pb[i]);
             }
             store_tile32<H, SPLIT, F16>(act, C::ACT_HALF, trow, c0, sv);
             if (valid && (st.flags & EF_STORE_A)) store_bf32<SPLIT, F16>(st.scr_a + (size_t)r * H + c0, st.lo_off, sv);
-            if (valid && (st.flags & EF_STORE_S)) store_bf32<SPLIT, F16>(st.scr_s + (size_t)r * H + c0, st.lo_off, dv);
           }
           wrote_act = true;
         } else if (st.epi == EPI_LN_FWD || st.epi == EPI_LN_BWD) {
           // z = acc + b; two-pass mean / variance over the H columns of this row
           float sum = 0.f;
 #pragma unroll 1
-          for (int c0 = 0; c0 < H; c0 += 32) {
-            tmem_ld32(tl + c0, v);
+          for (int cc = 0; cc < NC; ++cc) {
+            tmem_ld32(tl + cc * 32, v);
+            load_f32x32_ro(st.bias + cb + cc * 32, pb);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) sum += v[i] + __ldg(st.bias + c0 + i);
+            for (int i = 0; i < 32; ++i) sum += v[i] + pb[i];
           }
-          const float mean = sum * (1.0f / H);
+          const float mean = row_sum(sum) * (1.0f / H);
           float sq = 0.f;
 #pragma unroll 1
-          for (int c0 = 0; c0 < H; c0 += 32) {
-            tmem_ld32(tl + c0, v);
+          for (int cc = 0; cc < NC; ++cc) {
+            tmem_ld32(tl + cc * 32, v);
+            load_f32x32_ro(st.bias + cb + cc * 32, pb);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) { float d = v[i] + __ldg(st.bias + c0 + i) - mean; sq += d * d; }
+            for (int i = 0; i < 32; ++i) { float d = v[i] + pb[i] - mean; sq += d * d; }
           }
-          const float rstd = rsqrtf(sq * (1.0f / H) + p.eps);
+          const float rstd = rsqrtf(row_sum(sq) * (1.0f / H) + p.eps);
           if (st.epi == EPI_LN_FWD) {
 #pragma unroll 1
-            for (int c0 = 0; c0 < H; c0 += 32) {
-              tmem_ld32(tl + c0, v);
-              float res[32];
-              if (valid) load_f32x32(st.f_in + (size_t)r * st.ld_in + c0, res);
+            for (int cc = 0; cc < NC; ++cc) {
+              const int c0 = cb + cc * 32;
+              tmem_ld32(tl + cc * 32, v);
+              float res[32], gm[32], bt[32];
+              load_f32x32_ro(st.bias + c0, pb);
+              load_f32x32_ro(st.gamma + c0, gm);
+              load_f32x32_ro(st.beta + c0, bt);
+              if (valid && (st.flags & EF_RES16)) load_bf32<SPLIT, F16>(st.res16 + (size_t)r * H + c0, st.res16_lo, res);
+              else if (valid) load_f32x32(st.f_in + (size_t)r * st.ld_in + c0, res);
               else {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) res[i] = 0.f;
               }
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
-                float xh = (v[i] + __ldg(st.bias + c0 + i) - mean) * rstd;
-                v[i] = res[i] + fmaf(__ldg(st.gamma + c0 + i), xh, __ldg(st.beta + c0 + i));
+                float xh = (v[i] + pb[i] - mean) * rstd;
+                v[i] = res[i] + fmaf(gm[i], xh, bt[i]);
               }
               if (valid) {
-                store_f32x32(st.f_out + (size_t)r * st.ld_out + c0, v);
+                if (st.flags & EF_STORE_F32) store_f32x32(st.f_out + (size_t)r * st.ld_out + c0, v);
                 if (st.flags & EF_STORE_BF) store_bf32<SPLIT, F16>(st.bf_out + (size_t)r * H + c0, st.bf_lo, v);
               }
               if (st.flags & EF_WRITE_ACT) store_tile32<H, SPLIT, F16>(act, C::ACT_HALF, trow, c0, v);
@@ -432,25 +540,18 @@ __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainP
             const bool has_g = valid && r < st.valid_in;
             float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-            for (int cc = 0; cc < H / 32; ++cc) {
-              const int c0 = cc * 32;
-              tmem_ld32(tl + c0, v);
-              float dy[32], ga[32];
-              if (has_g) load_f32x32(st.f_in + (size_t)r * st.ld_in + c0, dy);
-              else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) dy[i] = 0.f;
-              }
-              if (valid && (st.flags & EF_GATHER_G)) {
-                load_f32x32(st.gather + (size_t)dst * H + c0, ga);
-#pragma unroll
-                for (int i = 0; i < 32; ++i) dy[i] += ga[i];
-              }
+            for (int cc = 0; cc < NC; ++cc) {
+              const int c0 = cb + cc * 32;
+              tmem_ld32(tl + cc * 32, v);
+              float dy[32], gm[32];
+              load_f32x32_ro(st.bias + c0, pb);
+              load_f32x32_ro(st.gamma + c0, gm);
+              load_dy(st, has_g, valid, r, dst, c0, dy);
               float t1[32], t2[32];
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
-                float xh = (v[i] + __ldg(st.bias + c0 + i) - mean) * rstd;
-                float dxh = dy[i] * __ldg(st.gamma + c0 + i);
+                float xh = (v[i] + pb[i] - mean) * rstd;
+                float dxh = dy[i] * gm[i];
                 s1 += dxh;
                 s2 += dxh * xh;
                 t1[i] = valid ? dy[i] * xh : 0.f;
@@ -459,27 +560,20 @@ __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainP
               colacc[0][cc] += warp_colsum32(t1);   // dgamma
               colacc[1][cc] += warp_colsum32(t2);   // dbeta
             }
-            s1 *= (1.0f / H);
-            s2 *= (1.0f / H);
+            s1 = row_sum(s1) * (1.0f / H);
+            s2 = row_sum(s2) * (1.0f / H);
 #pragma unroll
-            for (int cc = 0; cc < H / 32; ++cc) {
-              const int c0 = cc * 32;
-              tmem_ld32(tl + c0, v);
-              float dy[32], ga[32];
-              if (has_g) load_f32x32(st.f_in + (size_t)r * st.ld_in + c0, dy);
-              else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) dy[i] = 0.f;
-              }
-              if (valid && (st.flags & EF_GATHER_G)) {
-                load_f32x32(st.gather + (size_t)dst * H + c0, ga);
-#pragma unroll
-                for (int i = 0; i < 32; ++i) dy[i] += ga[i];
-              }
+            for (int cc = 0; cc < NC; ++cc) {
+              const int c0 = cb + cc * 32;
+              tmem_ld32(tl + cc * 32, v);
+              float dy[32], gm[32];
+              load_f32x32_ro(st.bias + c0, pb);
+              load_f32x32_ro(st.gamma + c0, gm);
+              load_dy(st, has_g, valid, r, dst, c0, dy);
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
-                float xh = (v[i] + __ldg(st.bias + c0 + i) - mean) * rstd;
-                float dxh = dy[i] * __ldg(st.gamma + c0 + i);
+                float xh = (v[i] + pb[i] - mean) * rstd;
+                float dxh = dy[i] * gm[i];
                 v[i] = valid ? rstd * (dxh - s1 - xh * s2) : 0.f;
               }
               store_tile32<H, SPLIT, F16>(act, C::ACT_HALF, trow, c0, v);
@@ -491,9 +585,9 @@ __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainP
         } else if (st.epi == EPI_DSILU) {
           if constexpr (BWD) {
 #pragma unroll
-            for (int cc = 0; cc < H / 32; ++cc) {
-              const int c0 = cc * 32;
-              tmem_ld32(tl + c0, v);
+            for (int cc = 0; cc < NC; ++cc) {
+              const int c0 = cb + cc * 32;
+              tmem_ld32(tl + cc * 32, v);
               float sd[32];
               if (valid) load_bf32<SPLIT, F16>(st.scr_s + (size_t)r * H + c0, st.lo_off, sd);
 #pragma unroll
@@ -508,15 +602,21 @@ __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainP
           }
         } else if (st.epi == EPI_STORE) {
 #pragma unroll 1
-          for (int c0 = 0; c0 < H; c0 += 32) {
-            tmem_ld32(tl + c0, v);
-            if (valid) store_f32x32(st.f_out + (size_t)r * st.ld_out + st.col0 + c0, v);
+          for (int cc = 0; cc < NC; ++cc) {
+            tmem_ld32(tl + cc * 32, v);
+            if (valid) {
+              if (st.flags & EF_OUT16)
+                store_bf32<SPLIT, F16>(st.bf_out + (size_t)r * st.ld_out + st.col0 + cb + cc * 32, st.bf_lo, v);
+              else
+                store_f32x32(st.f_out + (size_t)r * st.ld_out + st.col0 + cb + cc * 32, v);
+            }
           }
         } else if (st.epi == EPI_ADD) {
           const bool has_in = valid && r < st.valid_in;
 #pragma unroll 1
-          for (int c0 = 0; c0 < H; c0 += 32) {
-            tmem_ld32(tl + c0, v);
+          for (int cc = 0; cc < NC; ++cc) {
+            const int c0 = cb + cc * 32;
+            tmem_ld32(tl + cc * 32, v);
             if (valid) {
               float t[32];
               if (has_in) {
@@ -535,23 +635,27 @@ __global__ void __launch_bounds__(256, 1) k_chain(const __grid_constant__ ChainP
         }
         tc_fence_before();
         if (wrote_act) fence_proxy_async_smem();
-        mbar_arrive(acc_empty);
-        if (wrote_act) mbar_arrive(act_full);
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive_cluster(acc_empty_l);
+          if (wrote_act) mbar_arrive_cluster(act_full_l);
+        }
       }
     }
     if constexpr (BWD) {
       if (p.colsum) {
-        float* out = p.colsum + ((size_t)blockIdx.x * 4 + q) * NV_MAX * H;
+        float* out = p.colsum + ((size_t)blockIdx.x * 4 + q) * NV_MAX * H + cb;
 #pragma unroll
         for (int a = 0; a < NV_MAX; ++a)
 #pragma unroll
-          for (int b = 0; b < H / 32; ++b) out[a * H + b * 32 + lane] = colacc[a][b];
+          for (int b = 0; b < NC; ++b) out[a * H + b * 32 + lane] = colacc[a][b];
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (w == 2) tmem_dealloc(tmem, C::TMEM_COLS);
+  cluster_sync();
+  if (w == 2) tmem_dealloc_cg2(tmem, C::TMEM_COLS);
 }
 
 }  // namespace xmgn

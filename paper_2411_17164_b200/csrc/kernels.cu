@@ -51,9 +51,10 @@ __global__ void k_to_bf16(const float* __restrict__ in, __nv_bfloat16* __restric
 // warp per destination, lanes over 16-byte channel slices; output BF16 hi[+lo]
 // (the node GEMM operand and the layer checkpoint).  HBM-bound.
 template <int H, bool F16>
-__global__ void __launch_bounds__(256) k_aggregate(const int* __restrict__ off, const float* __restrict__ e,
-                                                   __nv_bfloat16* __restrict__ a, long long lo_off, int n) {
-  constexpr int V = H / 4 / 32;  // float4 per lane
+__global__ void __launch_bounds__(256) k_aggregate(const int* __restrict__ off, const __nv_bfloat16* __restrict__ e,
+                                                   long long e_lo, __nv_bfloat16* __restrict__ a, long long lo_off,
+                                                   int n) {
+  constexpr int V = H / 4 / 32;  // 4-element groups per lane
   const int lane = threadIdx.x & 31;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
     float4 acc[V];
@@ -61,11 +62,18 @@ __global__ void __launch_bounds__(256) k_aggregate(const int* __restrict__ off, 
     for (int v = 0; v < V; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int k0 = off[i], k1 = off[i + 1];
     for (int k = k0; k < k1; ++k) {
-      const float4* row = reinterpret_cast<const float4*>(e + (size_t)k * H);
+      const uint2* row = reinterpret_cast<const uint2*>(e + (size_t)k * H);
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        float4 x = __ldcs(row + lane + 32 * v);
-        acc[v].x += x.x; acc[v].y += x.y; acc[v].z += x.z; acc[v].w += x.w;
+        float x[4];
+        unpack4<F16>(row[lane + 32 * v], x);
+        if (e_lo) {
+          float y[4];
+          unpack4<false>(reinterpret_cast<const uint2*>(e + e_lo + (size_t)k * H)[lane + 32 * v], y);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) x[t] += y[t];
+        }
+        acc[v].x += x[0]; acc[v].y += x[1]; acc[v].z += x[2]; acc[v].w += x[3];
       }
     }
 #pragma unroll
@@ -284,17 +292,18 @@ void launch_to_bf16(bool f16, const float* in, __nv_bfloat16* out, long long lo_
   else k_to_bf16<false><<<blocks, 256, 0, st>>>(in, out, lo_off, n8);
 }
 template <bool F16>
-static void agg_t(int H, const int* off, const float* e, __nv_bfloat16* a, long long lo_off, int n, cudaStream_t st) {
+static void agg_t(int H, const int* off, const __nv_bfloat16* e, long long e_lo, __nv_bfloat16* a, long long lo_off,
+                  int n, cudaStream_t st) {
   int blocks = std::min((n + 7) / 8, 148 * 16);
-  if (H == 128) k_aggregate<128, F16><<<blocks, 256, 0, st>>>(off, e, a, lo_off, n);
-  else if (H == 256) k_aggregate<256, F16><<<blocks, 256, 0, st>>>(off, e, a, lo_off, n);
-  else k_aggregate<512, F16><<<blocks, 256, 0, st>>>(off, e, a, lo_off, n);
+  if (H == 128) k_aggregate<128, F16><<<blocks, 256, 0, st>>>(off, e, e_lo, a, lo_off, n);
+  else if (H == 256) k_aggregate<256, F16><<<blocks, 256, 0, st>>>(off, e, e_lo, a, lo_off, n);
+  else k_aggregate<512, F16><<<blocks, 256, 0, st>>>(off, e, e_lo, a, lo_off, n);
 }
-void launch_aggregate(bool f16, int H, const int* off, const float* e, __nv_bfloat16* a, long long lo_off, int n,
-                      cudaStream_t st) {
+void launch_aggregate(bool f16, int H, const int* off, const __nv_bfloat16* e, long long e_lo, __nv_bfloat16* a,
+                      long long lo_off, int n, cudaStream_t st) {
   if (n <= 0) return;
   count_launch();
-  if (f16) agg_t<true>(H, off, e, a, lo_off, n, st); else agg_t<false>(H, off, e, a, lo_off, n, st);
+  if (f16) agg_t<true>(H, off, e, e_lo, a, lo_off, n, st); else agg_t<false>(H, off, e, e_lo, a, lo_off, n, st);
 }
 template <bool F16>
 static void seg_t(int H, const int* off, const int* rev, const __nv_bfloat16* dz, long long dz_lo, __nv_bfloat16* D,

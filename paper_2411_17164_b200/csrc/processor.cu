@@ -49,8 +49,9 @@ struct xmgn_workspace {
   xmgn::PackJob* d_jobs = nullptr;
   int njobs = 0;
   // checkpoints (per layer) and live streams
-  xmgn::BfBuf e_ck, h_ck, a_ck;   // [L][Emax|Nmax][H]
-  float *e_buf[2] = {nullptr, nullptr}, *h_buf[2] = {nullptr, nullptr}, *P = nullptr;
+  xmgn::BfBuf e_ck, h_ck, a_ck;   // e_ck [L+1][Emax][H] (the 16-bit edge stream), h_ck / a_ck [L][Nmax][H]
+  float *h_buf[2] = {nullptr, nullptr};
+  xmgn::BfBuf P;                  // node pre-projection [Nmax][2H], 16-bit
   // backward
   float *Ge = nullptr, *Gh = nullptr, *Ga = nullptr;
   xmgn::BfBuf scrA[2], scrS[2], scrZ[3], D;
@@ -199,18 +200,23 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
     }
   }
   // weight maps
-  const int NB = ws->H < 256 ? ws->H : 256;
+  const int NB = (ws->H < 256 ? ws->H : 256) / 2;   // B rows per CTA of a pair
   const long long r1 = (long long)ws->L * ws->S1 * ws->H, r2 = (long long)ws->L * ws->S2 * ws->H;
   p.maps[0] = tmap_bf16(ws->wk1.p, ws->H, r1, ws->H, 64, NB);
   p.maps[1] = ws->split ? tmap_bf16(ws->wk1.p + ws->wk1.lo, ws->H, r1, ws->H, 64, NB) : p.maps[0];
   p.maps[2] = tmap_bf16(ws->wk2.p, 2 * ws->H, r2, 2 * ws->H, 64, NB);
   p.maps[3] = ws->split ? tmap_bf16(ws->wk2.p + ws->wk2.lo, 2 * ws->H, r2, 2 * ws->H, 64, NB) : p.maps[2];
-  const int tiles = (M + 127) / 128;
-  const int grid = tiles < ws->sms ? tiles : ws->sms;
+  const int pair_tiles = (M + 255) / 256;
+  const int grid = 2 * (pair_tiles < ws->sms / 2 ? pair_tiles : ws->sms / 2);
   p.colsum = bwd ? ws->colsum : nullptr;
   ProfScope ps(name, st);
   launch_chain(ws->H, ws->split, ws->f16, bwd, p, grid, st);
   XMGN_CUDA(cudaGetLastError(), "chain kernel launch");
+}
+
+static int chain_grid(xmgn_workspace* ws, int M) {
+  const int pair_tiles = (M + 255) / 256;
+  return 2 * (pair_tiles < ws->sms / 2 ? pair_tiles : ws->sms / 2);
 }
 
 static void set_a(xmgn_workspace* ws, Prog& pr, int slot, const BfBuf& b, long long rows, int width) {
@@ -333,14 +339,11 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
       ws->njobs = (int)jobs.size();
       ws->d_jobs = (PackJob*)dalloc(ws, jobs.size() * sizeof(PackJob));
       XMGN_CUDA(cudaMemcpy(ws->d_jobs, jobs.data(), jobs.size() * sizeof(PackJob), cudaMemcpyHostToDevice), "upload");
-      ws->e_ck = bfalloc(ws, (size_t)L * EH);
+      ws->e_ck = bfalloc(ws, (size_t)(L + 1) * EH);
       ws->h_ck = bfalloc(ws, (size_t)L * NH);
       ws->a_ck = bfalloc(ws, (size_t)L * NH);
-      for (int i = 0; i < 2; ++i) {
-        ws->e_buf[i] = (float*)dalloc(ws, EH * 4);
-        ws->h_buf[i] = (float*)dalloc(ws, NH * 4);
-      }
-      ws->P = (float*)dalloc(ws, 2 * NH * 4);
+      for (int i = 0; i < 2; ++i) ws->h_buf[i] = (float*)dalloc(ws, NH * 4);
+      ws->P = bfalloc(ws, 2 * NH);
       ws->Ge = (float*)dalloc(ws, EH * 4);
       ws->Gh = (float*)dalloc(ws, NH * 4);
       ws->Ga = (float*)dalloc(ws, NH * 4);
@@ -400,7 +403,8 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
         Step& s = pr.add();
         s.a_src = A_TMA; s.a_map0 = 4; s.K = H;
         s.b_map = W1; s.b_row0 = r1(0, half ? SL_PDT : SL_PST);
-        s.epi = EPI_STORE; s.f_out = ws->P; s.ld_out = 2 * H; s.col0 = half * H;
+        s.epi = EPI_STORE; s.flags = EF_OUT16; s.bf_out = ws->P.p; s.bf_lo = ws->P.lo; s.ld_out = 2 * H;
+        s.col0 = half * H;
       }
       run_prog(ws, "chain_proj", pr, (int)n0, nullptr, nullptr, false, st);
     }
@@ -408,9 +412,8 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
     for (int l = 1; l <= L; ++l) {
       const int li = l - 1;
       const int64_t nl = n_at(P, L, l), el = e_at(P, L, l);
-      const float* e_in = l == 1 ? e0 : ws->e_buf[cur];
       const float* h_in = l == 1 ? h0 : ws->h_buf[cur];
-      float* e_out = ws->e_buf[cur ^ 1];
+      BfBuf eck_next = at(ws->e_ck, (long long)l * EH);
       float* hn = l == L ? h_out : ws->h_buf[cur ^ 1];
       BfBuf eck_prev = at(ws->e_ck, (long long)li * EH), hck_prev = at(ws->h_ck, (long long)li * NH);
       BfBuf ack = at(ws->a_ck, (long long)li * NH);
@@ -422,19 +425,21 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
           s.a_src = j == 0 ? A_TMA : A_ACT; s.a_map0 = 4; s.K = H;
           s.b_map = W1; s.b_row0 = r1(li, j == 0 ? SL_E1T : SL_EJT + j - 1);
           s.epi = EPI_SILU; s.bias = params + Ly.b(li, 0, j);
-          if (j == 0) { s.flags |= EF_GATHER_P; s.gather = ws->P; }
+          if (j == 0) { s.flags |= EF_GATHER_P; s.gather16 = ws->P.p; s.gather16_lo = ws->P.lo; }
         }
+        // e^l = e^{l-1} + LN(..): the edge stream itself is 16-bit (checkpoint = next operand)
         Step& s = pr.add();
         s.a_src = A_ACT; s.K = H; s.b_map = W1; s.b_row0 = r1(li, SL_EJT + m - 1);
         s.epi = EPI_LN_FWD; s.bias = params + Ly.b(li, 0, m);
         s.gamma = params + Ly.gamma(li, 0); s.beta = params + Ly.beta(li, 0);
-        s.f_in = e_in; s.ld_in = H; s.f_out = e_out; s.ld_out = H;
-        if (l < L) { s.flags |= EF_STORE_BF; s.bf_out = ws->e_ck.p + (long long)l * EH; s.bf_lo = ws->e_ck.lo; }
+        s.flags = EF_RES16 | EF_STORE_BF;
+        s.res16 = eck_prev.p; s.res16_lo = eck_prev.lo;
+        s.bf_out = eck_next.p; s.bf_lo = eck_next.lo;
         run_prog(ws, "chain_edge_fwd", pr, (int)el, dp.src, dp.dst, false, st);
       }
       // aggregation (Eq. 2) -> a^l (BF16 operand + checkpoint)
       { ProfScope ps("aggregate", st);
-      launch_aggregate(ws->f16, H, dp.off, e_out, ack.p, ack.lo, (int)nl, st); }
+      launch_aggregate(ws->f16, H, dp.off, eck_next.p, eck_next.lo, ack.p, ack.lo, (int)nl, st); }
       XMGN_CUDA(cudaGetLastError(), "aggregate launch");
       {  // node update (Eq. 3) [+ P for layer l+1]
         Prog pr;
@@ -452,13 +457,15 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
         s.epi = EPI_LN_FWD; s.bias = params + Ly.b(li, 1, m);
         s.gamma = params + Ly.gamma(li, 1); s.beta = params + Ly.beta(li, 1);
         s.f_in = h_in; s.ld_in = H; s.f_out = hn; s.ld_out = H;
+        s.flags = EF_STORE_F32;
         if (l < L) {
           s.flags |= EF_STORE_BF | EF_WRITE_ACT;
           s.bf_out = ws->h_ck.p + (long long)l * NH; s.bf_lo = ws->h_ck.lo;
           for (int half = 0; half < 2; ++half) {
             Step& q = pr.add();
             q.a_src = A_ACT; q.K = H; q.b_map = W1; q.b_row0 = r1(l, half ? SL_PDT : SL_PST);
-            q.epi = EPI_STORE; q.f_out = ws->P; q.ld_out = 2 * H; q.col0 = half * H;
+            q.epi = EPI_STORE; q.flags = EF_OUT16; q.bf_out = ws->P.p; q.bf_lo = ws->P.lo; q.ld_out = 2 * H;
+            q.col0 = half * H;
           }
         }
         run_prog(ws, "chain_node_fwd", pr, (int)nl, nullptr, nullptr, false, st);
@@ -499,7 +506,6 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
       const int64_t enext = l < L ? e_at(P, L, l + 1) : 0;
       BfBuf eck = at(ws->e_ck, (long long)li * EH), hck = at(ws->h_ck, (long long)li * NH);
       BfBuf ack = at(ws->a_ck, (long long)li * NH);
-      const int tiles_n = (int)((nl + 127) / 128), tiles_e = (int)((el + 127) / 128);
       // common recompute + dgrad program of an MLP block (blk 0 edge, 1 node)
       auto mlp_bwd = [&](Prog& pr, int blk) {
         for (int j = 0; j < m; ++j) {
@@ -513,7 +519,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
           s.epi = EPI_SILU; s.bias = params + Ly.b(li, blk, j);
           s.flags = EF_STORE_A | EF_STORE_S;
           s.scr_a = ws->scrA[j].p; s.scr_s = ws->scrS[j].p; s.lo_off = ws->scrA[j].lo;
-          if (j == 0 && blk == 0) { s.flags |= EF_GATHER_P; s.gather = ws->P; }
+          if (j == 0 && blk == 0) { s.flags |= EF_GATHER_P; s.gather16 = ws->P.p; s.gather16_lo = ws->P.lo; }
         }
         Step& s = pr.add();
         s.a_src = A_ACT; s.K = H; s.b_map = W1; s.b_row0 = r1(li, (blk ? sl_njt(m) : SL_EJT) + m - 1);
@@ -542,7 +548,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         b.a_src = A_ACT; b.K = H; b.b_map = W1; b.b_row0 = r1(li, sl_n1a(m));
         b.epi = EPI_STORE; b.f_out = ws->Ga; b.ld_out = H; b.col0 = 0;
         run_prog(ws, "chain_node_bwd", pr, (int)nl, nullptr, nullptr, true, st);
-        colsum_reduce(ws, 1, li, grad_params, std::min(tiles_n, ws->sms), st);
+        colsum_reduce(ws, 1, li, grad_params, chain_grid(ws, (int)nl), st);
         wgrad(ws, hck, ack, H, H / 128, ws->scrZ[0], H, 0, nl, 2 * H, grad_params, Ly.W(li, 1, 0), st);
         for (int j = 1; j <= m; ++j)
           wgrad(ws, ws->scrA[j - 1], none, H, H / 128, ws->scrZ[j], H, 0, nl, H, grad_params, Ly.W(li, 1, j), st);
@@ -554,7 +560,8 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
           Step& s = pr.add();
           s.a_src = A_TMA; s.a_map0 = 4; s.K = H;
           s.b_map = W1; s.b_row0 = r1(li, half ? SL_PDT : SL_PST);
-          s.epi = EPI_STORE; s.f_out = ws->P; s.ld_out = 2 * H; s.col0 = half * H;
+          s.epi = EPI_STORE; s.flags = EF_OUT16; s.bf_out = ws->P.p; s.bf_lo = ws->P.lo; s.ld_out = 2 * H;
+          s.col0 = half * H;
         }
         run_prog(ws, "chain_proj", pr, (int)nprev, nullptr, nullptr, false, st);
       }
@@ -567,7 +574,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         a.epi = EPI_ADD; a.f_in = ws->Ge; a.f_out = ws->Ge; a.ld_in = a.ld_out = H; a.valid_in = (int)enext;
         a.flags = EF_GATHER_G; a.gather = ws->Ga;
         run_prog(ws, "chain_edge_bwd", pr, (int)el, dp.src, dp.dst, true, st);
-        colsum_reduce(ws, 0, li, grad_params, std::min(tiles_e, ws->sms), st);
+        colsum_reduce(ws, 0, li, grad_params, chain_grid(ws, (int)el), st);
         wgrad(ws, eck, none, H, H / 128, ws->scrZ[0], H, 0, el, H, grad_params, Ly.W(li, 0, 0), st);
         for (int j = 1; j <= m; ++j)
           wgrad(ws, ws->scrA[j - 1], none, H, H / 128, ws->scrZ[j], H, 0, el, H, grad_params, Ly.W(li, 0, j), st);
