@@ -46,7 +46,9 @@ enum : int {
   EF_STORE_BF = 32,    // EPI_LN_FWD: write bf16 output (checkpoint)
   EF_RES16 = 64,       // EPI_LN_FWD: residual input is the 16-bit tensor res16 (else fp32 f_in)
   EF_STORE_F32 = 128,  // EPI_LN_FWD: write the fp32 output f_out
-  EF_OUT16 = 256       // EPI_STORE: write 16-bit bf_out (ld_out, col0) instead of fp32 f_out
+  EF_OUT16 = 256,      // EPI_STORE: write 16-bit bf_out (ld_out, col0) instead of fp32 f_out
+  EF_G16 = 512         // EPI_LN_BWD / EPI_ADD: the gradient stream is the 16-bit g16 (edge programs):
+                       // LN_BWD writes dY = g16 (+ ga16[dst]) back into g16; ADD does g16 += acc
 };
 
 enum : int {
@@ -77,6 +79,10 @@ struct Step {
   long long res16_lo;
   const __nv_bfloat16* gather16;  // 16-bit P [N][2H] (EF_GATHER_P); lo at + gather16_lo
   long long gather16_lo;
+  __nv_bfloat16* g16;             // 16-bit gradient stream [rows][H] (EF_G16)
+  long long g16_lo;
+  const __nv_bfloat16* ga16;      // 16-bit aggregation adjoint G_a [N][H] gathered by dst (EF_G16)
+  long long ga16_lo;
 };
 
 constexpr int MAX_STEPS = 8;
@@ -197,6 +203,27 @@ __device__ __forceinline__ void load_bf32(const __nv_bfloat16* p, long long lo_o
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[q * 8 + i] += t[i];
     }
+  }
+}
+// v <- value as stored by store_bf32 (16-bit hi [+ lo]) -- keeps passes bitwise consistent
+template <bool SPLIT, bool F16>
+__device__ __forceinline__ void load_bf32_regs(float* v) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {
+    uint32_t hi, lo;
+    split2<F16, SPLIT>(v[i], v[i + 1], hi, lo);
+    float t[8];
+    uint4 u = make_uint4(hi, 0, 0, 0);
+    unpack8<F16 && !SPLIT>(u, t);
+    float a = t[0], b = t[1];
+    if constexpr (SPLIT) {
+      uint4 w = make_uint4(lo, 0, 0, 0);
+      unpack8<false>(w, t);
+      a += t[0];
+      b += t[1];
+    }
+    v[i] = a;
+    v[i + 1] = b;
   }
 }
 __device__ __forceinline__ void load_f32x32(const float* p, float* v) {
@@ -546,7 +573,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
               float dy[32], gm[32];
               load_f32x32_ro(st.bias + c0, pb);
               load_f32x32_ro(st.gamma + c0, gm);
-              load_dy(st, has_g, valid, r, dst, c0, dy);
+              if (st.flags & EF_G16) {
+                // dY = G_e (rows < valid_in) + G_a[dst]; written back as G_e' for pass B and dX
+                float ga[32];
+                if (has_g) load_bf32<SPLIT, F16>(st.g16 + (size_t)r * H + c0, st.g16_lo, dy);
+                else {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) dy[i] = 0.f;
+                }
+                if (valid) {
+                  load_bf32<SPLIT, F16>(st.ga16 + (size_t)dst * H + c0, st.ga16_lo, ga);
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) dy[i] += ga[i];
+                  store_bf32<SPLIT, F16>(st.g16 + (size_t)r * H + c0, st.g16_lo, dy);
+                  // use the stored (rounded) value so pass B and this pass agree
+                  load_bf32_regs<SPLIT, F16>(dy);
+                }
+              } else {
+                load_dy(st, has_g, valid, r, dst, c0, dy);
+              }
               float t1[32], t2[32];
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
@@ -569,7 +614,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
               float dy[32], gm[32];
               load_f32x32_ro(st.bias + c0, pb);
               load_f32x32_ro(st.gamma + c0, gm);
-              load_dy(st, has_g, valid, r, dst, c0, dy);
+              if (st.flags & EF_G16) {
+                if (valid) load_bf32<SPLIT, F16>(st.g16 + (size_t)r * H + c0, st.g16_lo, dy);
+                else {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) dy[i] = 0.f;
+                }
+              } else {
+                load_dy(st, has_g, valid, r, dst, c0, dy);
+              }
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
                 float xh = (v[i] + pb[i] - mean) * rstd;
@@ -609,6 +662,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
                 store_bf32<SPLIT, F16>(st.bf_out + (size_t)r * st.ld_out + st.col0 + cb + cc * 32, st.bf_lo, v);
               else
                 store_f32x32(st.f_out + (size_t)r * st.ld_out + st.col0 + cb + cc * 32, v);
+            }
+          }
+        } else if (st.epi == EPI_ADD && (st.flags & EF_G16)) {
+#pragma unroll 1
+          for (int cc = 0; cc < NC; ++cc) {
+            const int c0 = cb + cc * 32;
+            tmem_ld32(tl + cc * 32, v);
+            if (valid) {
+              float t[32];
+              load_bf32<SPLIT, F16>(st.g16 + (size_t)r * H + c0, st.g16_lo, t);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] += t[i];
+              store_bf32<SPLIT, F16>(st.g16 + (size_t)r * H + c0, st.g16_lo, v);
             }
           }
         } else if (st.epi == EPI_ADD) {

@@ -46,6 +46,24 @@ __global__ void k_to_bf16(const float* __restrict__ in, __nv_bfloat16* __restric
   }
 }
 
+// ---------------------------------------------------------------- 16-bit (hi [+ lo]) -> FP32
+template <bool F16>
+__global__ void k_to_f32(const __nv_bfloat16* __restrict__ in, long long lo_off, float* __restrict__ out,
+                         long long n8) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n8; t += (long long)gridDim.x * blockDim.x) {
+    float v[8];
+    unpack8<F16>(reinterpret_cast<const uint4*>(in)[t], v);
+    if (lo_off) {
+      float w[8];
+      unpack8<false>(reinterpret_cast<const uint4*>(in + lo_off)[t], w);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] += w[i];
+    }
+    reinterpret_cast<float4*>(out)[2 * t] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(out)[2 * t + 1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
 // ---------------------------------------------------------------- aggregation (Eq. 2)
 // a_i = sum_{k in [off_i, off_{i+1})} e'_k, FP32 accumulation in CSR order, one
 // warp per destination, lanes over 16-byte channel slices; output BF16 hi[+lo]
@@ -291,6 +309,15 @@ void launch_to_bf16(bool f16, const float* in, __nv_bfloat16* out, long long lo_
   if (f16) k_to_bf16<true><<<blocks, 256, 0, st>>>(in, out, lo_off, n8);
   else k_to_bf16<false><<<blocks, 256, 0, st>>>(in, out, lo_off, n8);
 }
+void launch_to_f32(bool f16, const __nv_bfloat16* in, long long lo_off, float* out, long long n, cudaStream_t st) {
+  if (n <= 0) return;
+  count_launch();
+  long long n8 = n / 8;
+  int blocks = (int)std::min<long long>((n8 + 255) / 256, 148 * 16);
+  if (f16 && !lo_off) k_to_f32<true><<<blocks, 256, 0, st>>>(in, lo_off, out, n8);
+  else k_to_f32<false><<<blocks, 256, 0, st>>>(in, lo_off, out, n8);
+}
+
 template <bool F16>
 static void agg_t(int H, const int* off, const __nv_bfloat16* e, long long e_lo, __nv_bfloat16* a, long long lo_off,
                   int n, cudaStream_t st) {

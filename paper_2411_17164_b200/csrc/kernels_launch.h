@@ -15,6 +15,7 @@ struct ColsumDst {
 
 // `f16`: the 16-bit operand buffers hold FP16 instead of BF16 (XMGN_PREC_FP16).
 void launch_pack(bool f16, const float* params, const PackJob* jobs, int njobs, cudaStream_t st);
+void launch_to_f32(bool f16, const __nv_bfloat16* in, long long lo_off, float* out, long long n, cudaStream_t st);
 void launch_to_bf16(bool f16, const float* in, __nv_bfloat16* out, long long lo_off, long long n, cudaStream_t st);
 void launch_aggregate(bool f16, int H, const int* off, const __nv_bfloat16* e, long long e_lo, __nv_bfloat16* a,
                       long long lo_off, int n, cudaStream_t st);

@@ -53,7 +53,8 @@ struct xmgn_workspace {
   float *h_buf[2] = {nullptr, nullptr};
   xmgn::BfBuf P;                  // node pre-projection [Nmax][2H], 16-bit
   // backward
-  float *Ge = nullptr, *Gh = nullptr, *Ga = nullptr;
+  float* Gh = nullptr;            // dL/dh (FP32, node level)
+  xmgn::BfBuf Ge, Ga;             // dL/de (16-bit edge stream), dL/da (16-bit)
   xmgn::BfBuf scrA[2], scrS[2], scrZ[3], D;
   float* part = nullptr;  // wgrad split-K partials
   int part_splits = 0;
@@ -344,9 +345,9 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
       ws->a_ck = bfalloc(ws, (size_t)L * NH);
       for (int i = 0; i < 2; ++i) ws->h_buf[i] = (float*)dalloc(ws, NH * 4);
       ws->P = bfalloc(ws, 2 * NH);
-      ws->Ge = (float*)dalloc(ws, EH * 4);
+      ws->Ge = bfalloc(ws, EH);
       ws->Gh = (float*)dalloc(ws, NH * 4);
-      ws->Ga = (float*)dalloc(ws, NH * 4);
+      ws->Ga = bfalloc(ws, NH);
       for (int j = 0; j < m; ++j) { ws->scrA[j] = bfalloc(ws, RH); ws->scrS[j] = bfalloc(ws, RH); }
       for (int j = 0; j <= m; ++j) ws->scrZ[j] = bfalloc(ws, RH);
       ws->D = bfalloc(ws, 2 * NH);
@@ -525,9 +526,12 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         s.a_src = A_ACT; s.K = H; s.b_map = W1; s.b_row0 = r1(li, (blk ? sl_njt(m) : SL_EJT) + m - 1);
         s.epi = EPI_LN_BWD; s.bias = params + Ly.b(li, blk, m);
         s.gamma = params + Ly.gamma(li, blk); s.beta = params + Ly.beta(li, blk);
-        s.f_in = blk ? ws->Gh : ws->Ge; s.ld_in = H;
+        s.f_in = ws->Gh; s.ld_in = H;
         s.valid_in = blk ? (int)nl : (int)enext;
-        if (blk == 0) { s.flags |= EF_GATHER_G; s.gather = ws->Ga; }
+        if (blk == 0) {
+          s.flags |= EF_G16;
+          s.g16 = ws->Ge.p; s.g16_lo = ws->Ge.lo; s.ga16 = ws->Ga.p; s.ga16_lo = ws->Ga.lo;
+        }
         s.scr_z = ws->scrZ[m].p; s.lo_off = ws->scrZ[m].lo;
         for (int j = m; j >= 1; --j) {
           Step& d = pr.add();
@@ -546,7 +550,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         a.epi = EPI_ADD; a.f_in = ws->Gh; a.f_out = ws->Gh; a.ld_in = a.ld_out = H; a.valid_in = (int)nl;
         Step& b = pr.add();   // da: G_a = dZ0 W0[agg rows]^T
         b.a_src = A_ACT; b.K = H; b.b_map = W1; b.b_row0 = r1(li, sl_n1a(m));
-        b.epi = EPI_STORE; b.f_out = ws->Ga; b.ld_out = H; b.col0 = 0;
+        b.epi = EPI_STORE; b.flags = EF_OUT16; b.bf_out = ws->Ga.p; b.bf_lo = ws->Ga.lo; b.ld_out = H; b.col0 = 0;
         run_prog(ws, "chain_node_bwd", pr, (int)nl, nullptr, nullptr, true, st);
         colsum_reduce(ws, 1, li, grad_params, chain_grid(ws, (int)nl), st);
         wgrad(ws, hck, ack, H, H / 128, ws->scrZ[0], H, 0, nl, 2 * H, grad_params, Ly.W(li, 1, 0), st);
@@ -571,8 +575,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         mlp_bwd(pr, 0);
         Step& a = pr.add();   // G_e^{l-1} = G_e' + dZ0 W0[e rows]^T
         a.a_src = A_ACT; a.K = H; a.b_map = W1; a.b_row0 = r1(li, sl_e1e(m));
-        a.epi = EPI_ADD; a.f_in = ws->Ge; a.f_out = ws->Ge; a.ld_in = a.ld_out = H; a.valid_in = (int)enext;
-        a.flags = EF_GATHER_G; a.gather = ws->Ga;
+        a.epi = EPI_ADD; a.flags = EF_G16; a.g16 = ws->Ge.p; a.g16_lo = ws->Ge.lo;
         run_prog(ws, "chain_edge_bwd", pr, (int)el, dp.src, dp.dst, true, st);
         colsum_reduce(ws, 0, li, grad_params, chain_grid(ws, (int)el), st);
         wgrad(ws, eck, none, H, H / 128, ws->scrZ[0], H, 0, el, H, grad_params, Ly.W(li, 0, 0), st);
@@ -602,7 +605,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         XMGN_CUDA(cudaMemsetAsync(grad_h0 + n0 * H, 0, (P.n_local - n0) * H * sizeof(float), st), "grad_h0");
     }
     if (grad_e0) {
-      XMGN_CUDA(cudaMemcpyAsync(grad_e0, ws->Ge, e1 * H * sizeof(float), cudaMemcpyDeviceToDevice, st), "grad_e0");
+      launch_to_f32(ws->f16, ws->Ge.p, ws->Ge.lo, grad_e0, e1 * H, st);
       if (P.e_local > e1)
         XMGN_CUDA(cudaMemsetAsync(grad_e0 + e1 * H, 0, (P.e_local - e1) * H * sizeof(float), st), "grad_e0");
     }
