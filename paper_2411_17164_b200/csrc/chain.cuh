@@ -47,6 +47,8 @@ enum : int {
   EF_RES16 = 64,       // EPI_LN_FWD: residual input is the 16-bit tensor res16 (else fp32 f_in)
   EF_STORE_F32 = 128,  // EPI_LN_FWD: write the fp32 output f_out
   EF_OUT16 = 256,      // EPI_STORE: write 16-bit bf_out (ld_out, col0) instead of fp32 f_out
+  EF_COLSUM_ALL = 1024,  // EPI_LN_BWD / EPI_DSILU: also accumulate dbeta / db column sums here
+                         // (else only dgamma; the bias sums come from the wgrad GEMMs)
   EF_G16 = 512         // EPI_LN_BWD / EPI_ADD: the gradient stream is the 16-bit g16 (edge programs):
                        // LN_BWD writes dY = g16 (+ ga16[dst]) back into g16; ADD does g16 += acc
 };
@@ -81,6 +83,7 @@ struct Step {
   long long gather16_lo;
   __nv_bfloat16* g16;             // 16-bit gradient stream [rows][H] (EF_G16)
   long long g16_lo;
+  __nv_bfloat16* g16_out;         // EPI_ADD + EF_G16 output (same lo offset as g16)
   const __nv_bfloat16* ga16;      // 16-bit aggregation adjoint G_a [N][H] gathered by dst (EF_G16)
   long long ga16_lo;
 };
@@ -339,11 +342,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
         for (int s = 0; s < p.n_steps; ++s, ++g) {
           const Step& st = p.steps[s];
           const bool tma_a = st.a_src == A_TMA;
-          if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) { mbar_wait_cluster(act_free, naf & 1); ++naf; }
+          if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) { mbar_wait(act_free, naf & 1); ++naf; }
           for (int kc = 0; kc < st.K / 64; ++kc) {
             if (tma_a) {
               const int slot = ai % C::SA;
-              if (ai >= C::SA) mbar_wait_cluster(&a_empty[slot], ((ai / C::SA) - 1) & 1);
+              if (ai >= C::SA) mbar_wait(&a_empty[slot], ((ai / C::SA) - 1) & 1);
               if (rank == 0) mbar_expect_tx(&a_full[slot], 2 * C::A_SLOT);
               const uint32_t fb = mapa_shared(smem_u32(&a_full[slot]), 0);
               uint8_t* dstp = act + slot * C::A_SLOT;
@@ -356,7 +359,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
             }
             for (int nh = 0; nh < NH; ++nh) {
               const int slot = bi % C::SB;
-              if (bi >= C::SB) mbar_wait_cluster(&b_empty[slot], ((bi / C::SB) - 1) & 1);
+              if (bi >= C::SB) mbar_wait(&b_empty[slot], ((bi / C::SB) - 1) & 1);
               if (rank == 0) mbar_expect_tx(&b_full[slot], 2 * C::B_SLOT);
               const uint32_t fb = mapa_shared(smem_u32(&b_full[slot]), 0);
               uint8_t* dstp = bring + slot * C::B_SLOT;
@@ -389,15 +392,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
             if (elect_one()) { mbar_arrive(act_free); mbar_arrive_cluster(act_free_peer); }
             __syncwarp();
           }
-          if (g > 0) mbar_wait_cluster(acc_empty, (g - 1) & 1);
-          if (st.ctl & CTL_WAIT_ACT) { mbar_wait_cluster(act_full, nact & 1); ++nact; }
+          if (g > 0) mbar_wait(acc_empty, (g - 1) & 1);
+          if (st.ctl & CTL_WAIT_ACT) { mbar_wait(act_full, nact & 1); ++nact; }
           tc_fence_after();
           for (int kc = 0; kc < st.K / 64; ++kc) {
             int aslot = 0;
             uint32_t a_base;
             if (tma_a) {
               aslot = ai % C::SA;
-              mbar_wait_cluster(&a_full[aslot], (ai / C::SA) & 1);
+              mbar_wait(&a_full[aslot], (ai / C::SA) & 1);
               a_base = smem_u32(act + aslot * C::A_SLOT);
             } else {
               a_base = smem_u32(act + kc * (128 * 128));
@@ -405,7 +408,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
             const uint32_t a_lo = tma_a ? C::A_SLOT_HALF : C::ACT_HALF;
             for (int nh = 0; nh < NH; ++nh) {
               const int bslot = bi % C::SB;
-              mbar_wait_cluster(&b_full[bslot], (bi / C::SB) & 1);
+              mbar_wait(&b_full[bslot], (bi / C::SB) & 1);
               tc_fence_after();
               const uint32_t b_base = smem_u32(bring + bslot * C::B_SLOT);
               if (elect_one()) {
@@ -603,7 +606,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
                 t2[i] = valid ? dy[i] : 0.f;
               }
               colacc[0][cc] += warp_colsum32(t1);   // dgamma
-              colacc[1][cc] += warp_colsum32(t2);   // dbeta
+              if (st.flags & EF_COLSUM_ALL) colacc[1][cc] += warp_colsum32(t2);   // dbeta
             }
             s1 = row_sum(s1) * (1.0f / H);
             s2 = row_sum(s2) * (1.0f / H);
@@ -631,7 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
               }
               store_tile32<H, SPLIT, F16>(act, C::ACT_HALF, trow, c0, v);
               if (valid) store_bf32<SPLIT, F16>(st.scr_z + (size_t)r * H + c0, st.lo_off, v);
-              colacc[2][cc] += warp_colsum32(v);    // db_{m+1}
+              if (st.flags & EF_COLSUM_ALL) colacc[2][cc] += warp_colsum32(v);    // db_{m+1}
             }
             wrote_act = true;
           }
@@ -647,9 +650,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
               for (int i = 0; i < 32; ++i) v[i] = valid ? v[i] * sd[i] : 0.f;
               store_tile32<H, SPLIT, F16>(act, C::ACT_HALF, trow, c0, v);
               if (valid) store_bf32<SPLIT, F16>(st.scr_z + (size_t)r * H + c0, st.lo_off, v);
-              const float cs = warp_colsum32(v);
-              if (st.vec0 == 3) colacc[3][cc] += cs;  // db_m
-              else colacc[4][cc] += cs;               // db_{m-1}
+              if (st.flags & EF_COLSUM_ALL) {
+                const float cs = warp_colsum32(v);
+                if (st.vec0 == 3) colacc[3][cc] += cs;  // db_m
+                else colacc[4][cc] += cs;               // db_{m-1}
+              }
             }
             wrote_act = true;
           }
@@ -674,7 +679,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
               load_bf32<SPLIT, F16>(st.g16 + (size_t)r * H + c0, st.g16_lo, t);
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] += t[i];
-              store_bf32<SPLIT, F16>(st.g16 + (size_t)r * H + c0, st.g16_lo, v);
+              store_bf32<SPLIT, F16>(st.g16_out + (size_t)r * H + c0, st.g16_lo, v);
             }
           }
         } else if (st.epi == EPI_ADD) {

@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(128, 1) k_wgrad(const __grid_constant__ WgradP
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
   const int w = warp_id();
   const int mt = blockIdx.x, nt = blockIdx.y, sp = blockIdx.z;
+  const bool ones = p.ones_tile && mt == p.Hin / 128;   // column sums of B (bias gradient)
   const CUtensorMap* am = mt < p.a_split_tiles ? &p.a0 : &p.a1;
   const CUtensorMap* aml = mt < p.a_split_tiles ? &p.a0lo : &p.a1lo;
   const int acol = (mt < p.a_split_tiles ? mt : mt - p.a_split_tiles) * 128;
@@ -197,6 +198,19 @@ __global__ void __launch_bounds__(128, 1) k_wgrad(const __grid_constant__ WgradP
     fence_barrier_init();
   }
   if (w == 2) tmem_alloc(tslot, NT);
+  if (ones) {
+    // A = all-ones (hi) / zeros (lo): layout-independent, written once for every stage
+    const uint32_t one = F16 ? 0x3C003C00u : 0x3F803F80u;
+    for (int s = 0; s < S; ++s) {
+      uint32_t* a = reinterpret_cast<uint32_t*>(smem + s * STAGE);
+      for (int i = threadIdx.x; i < (int)(A_HALF / 4); i += blockDim.x) a[i] = one;
+      if constexpr (SPLIT) {
+        uint32_t* al = reinterpret_cast<uint32_t*>(smem + s * STAGE + A_HALF + B_HALF);
+        for (int i = threadIdx.x; i < (int)(A_HALF / 4); i += blockDim.x) al[i] = 0u;
+      }
+    }
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -206,16 +220,20 @@ __global__ void __launch_bounds__(128, 1) k_wgrad(const __grid_constant__ WgradP
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % S;
         if (kb >= S) mbar_wait(&empty[s], ((kb / S) - 1) & 1);
-        mbar_expect_tx(&full[s], STAGE);
+        mbar_expect_tx(&full[s], ones ? F * B_HALF : STAGE);
         uint8_t* st = smem + s * STAGE;
         const int row = (c0 + kb) * 64;
-        tma_load_2d(st, am, &full[s], acol, row);
-        tma_load_2d(st + 8192, am, &full[s], acol + 64, row);
+        if (!ones) {
+          tma_load_2d(st, am, &full[s], acol, row);
+          tma_load_2d(st + 8192, am, &full[s], acol + 64, row);
+        }
         for (int j = 0; j < NT / 64; ++j) tma_load_2d(st + A_HALF + j * 8192, &p.b, &full[s], bcol + j * 64, row);
         if constexpr (SPLIT) {
           uint8_t* sl = st + A_HALF + B_HALF;
-          tma_load_2d(sl, aml, &full[s], acol, row);
-          tma_load_2d(sl + 8192, aml, &full[s], acol + 64, row);
+          if (!ones) {
+            tma_load_2d(sl, aml, &full[s], acol, row);
+            tma_load_2d(sl + 8192, aml, &full[s], acol + 64, row);
+          }
           for (int j = 0; j < NT / 64; ++j) tma_load_2d(sl + A_HALF + j * 8192, &p.blo, &full[s], bcol + j * 64, row);
         }
       }
@@ -248,7 +266,8 @@ __global__ void __launch_bounds__(128, 1) k_wgrad(const __grid_constant__ WgradP
   }
   __syncwarp();
   const int m = mt * 128 + w * 32 + lane_id();
-  float* out = p.part + ((size_t)sp * p.Hin + m) * p.Hout + nt * NT;
+  const int rows_out = p.Hin + (p.ones_tile ? 128 : 0);
+  float* out = p.part + ((size_t)sp * rows_out + m) * p.Hout + nt * NT;
   if (nk > 0) {
     mbar_wait(done, 0);
     tc_fence_after();
@@ -267,11 +286,12 @@ __global__ void __launch_bounds__(128, 1) k_wgrad(const __grid_constant__ WgradP
   if (w == 2) tmem_dealloc(tmem, NT);
 }
 
-// grad[i] += sum_{s < S} part[s][i]  (fixed order)
-__global__ void k_reduce_part(const float* __restrict__ part, int S, long long n, float* __restrict__ grad) {
+// grad[i] += sum_{s < S} part[s][i] for i < n, split stride `ld` (fixed order)
+__global__ void k_reduce_part(const float* __restrict__ part, int S, long long n, long long ld,
+                              float* __restrict__ grad) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     float s = 0.f;
-    for (int k = 0; k < S; ++k) s += part[k * n + i];
+    for (int k = 0; k < S; ++k) s += part[k * ld + i];
     grad[i] += s;
   }
 }
@@ -361,7 +381,7 @@ static void wgrad_launch(const WgradParams& p, dim3 grid, cudaStream_t st) {
 void launch_wgrad(const WgradParams& p, bool split, bool f16, cudaStream_t st) {
   count_launch();
   const int NT = p.Hout >= 256 ? 256 : p.Hout;
-  dim3 grid(p.Hin / 128, p.Hout / NT, p.n_split);
+  dim3 grid(p.Hin / 128 + (p.ones_tile ? 1 : 0), p.Hout / NT, p.n_split);
   if (NT == 256) {
     if (f16) wgrad_launch<256, false, true>(p, grid, st); else wgrad_launch<256, false, false>(p, grid, st);
   } else {
@@ -370,10 +390,10 @@ void launch_wgrad(const WgradParams& p, bool split, bool f16, cudaStream_t st) {
     else wgrad_launch<128, false, false>(p, grid, st);
   }
 }
-void launch_reduce_part(const float* part, int S, long long n, float* grad, cudaStream_t st) {
+void launch_reduce_part(const float* part, int S, long long n, long long ld, float* grad, cudaStream_t st) {
   count_launch();
   int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
-  k_reduce_part<<<blocks, 256, 0, st>>>(part, S, n, grad);
+  k_reduce_part<<<blocks, 256, 0, st>>>(part, S, n, ld, grad);
 }
 void launch_reduce_colsum(const float* part, int nblk, int nv, int H, ColsumDst d, float* grad, cudaStream_t st) {
   count_launch();

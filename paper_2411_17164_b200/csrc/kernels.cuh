@@ -22,7 +22,8 @@ struct WgradParams {
   int rows;             // reduction length (rows of the activation tensors)
   int n_split;          // split-K factor (gridDim.z)
   int Hin, Hout;        // dW is [Hin][Hout]
-  float* part;          // [n_split][Hin][Hout]
+  int ones_tile;        // 1: M tile Hin/128 uses A = ones -> its rows are the column sums of B (bias grads)
+  float* part;          // [n_split][Hin (+128)][Hout]
 };
 
 }  // namespace xmgn

@@ -22,7 +22,7 @@ void launch_aggregate(bool f16, int H, const int* off, const __nv_bfloat16* e, l
 void launch_segsum(bool f16, int H, const int* off, const int* rev, const __nv_bfloat16* dz, long long dz_lo,
                    __nv_bfloat16* D, long long d_lo, int n, int e_act, cudaStream_t st);
 void launch_wgrad(const WgradParams& p, bool split, bool f16, cudaStream_t st);
-void launch_reduce_part(const float* part, int S, long long n, float* grad, cudaStream_t st);
+void launch_reduce_part(const float* part, int S, long long n, long long ld, float* grad, cudaStream_t st);
 void launch_reduce_colsum(const float* part, int nblk, int nv, int H, ColsumDst d, float* grad, cudaStream_t st);
 void launch_nonfinite(const float* x, long long n, int* flag, cudaStream_t st);
 // profiling (processor.cu): every kernel launch of the library is counted;

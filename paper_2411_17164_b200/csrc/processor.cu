@@ -54,7 +54,7 @@ struct xmgn_workspace {
   xmgn::BfBuf P;                  // node pre-projection [Nmax][2H], 16-bit
   // backward
   float* Gh = nullptr;            // dL/dh (FP32, node level)
-  xmgn::BfBuf Ge, Ga;             // dL/de (16-bit edge stream), dL/da (16-bit)
+  xmgn::BfBuf Ge[2], Ga;          // dL/de (16-bit edge stream, ping-pong), dL/da (16-bit)
   xmgn::BfBuf scrA[2], scrS[2], scrZ[3], D;
   float* part = nullptr;  // wgrad split-K partials
   int part_splits = 0;
@@ -227,18 +227,23 @@ static void set_a(xmgn_workspace* ws, Prog& pr, int slot, const BfBuf& b, long l
 
 static BfBuf at(const BfBuf& b, long long elem) { return BfBuf{b.p + elem, b.lo}; }
 
-// weight-gradient GEMM + fixed-order reduction into grad[dst .. dst + Hin*Hout)
+// weight-gradient GEMM + fixed-order reduction into grad[dst .. dst + Hin*Hout); with
+// bias_dst >= 0 an extra all-ones A tile also yields grad[bias_dst + c] += sum_rows B[:, c].
+// Hin = 0 computes only that column sum.
 static void wgrad(xmgn_workspace* ws, const BfBuf& a0, const BfBuf& a1, int a_width, int a_split_tiles, const BfBuf& b,
-                  int b_width, int b_col0, long long rows, int Hin, float* grad, long long dst, cudaStream_t st) {
+                  int b_width, int b_col0, long long rows, int Hin, float* grad, long long dst, cudaStream_t st,
+                  long long bias_dst = -1) {
   if (rows <= 0) return;
   const int H = ws->H;
   WgradParams p;
   std::memset(&p, 0, sizeof(p));
-  p.a0 = tmap_bf16(a0.p, a_width, rows, a_width, 64, 64);
-  p.a0lo = ws->split ? tmap_bf16(a0.p + a0.lo, a_width, rows, a_width, 64, 64) : p.a0;
-  const BfBuf& a1r = a1.p ? a1 : a0;
-  p.a1 = tmap_bf16(a1r.p, a_width, rows, a_width, 64, 64);
-  p.a1lo = ws->split ? tmap_bf16(a1r.p + a1r.lo, a_width, rows, a_width, 64, 64) : p.a1;
+  const BfBuf& a0r = a0.p ? a0 : b;
+  const int aw = a0.p ? a_width : b_width;
+  p.a0 = tmap_bf16(a0r.p, aw, rows, aw, 64, 64);
+  p.a0lo = ws->split ? tmap_bf16(a0r.p + a0r.lo, aw, rows, aw, 64, 64) : p.a0;
+  const BfBuf& a1r = a1.p ? a1 : a0r;
+  p.a1 = tmap_bf16(a1r.p, aw, rows, aw, 64, 64);
+  p.a1lo = ws->split ? tmap_bf16(a1r.p + a1r.lo, aw, rows, aw, 64, 64) : p.a1;
   p.b = tmap_bf16(b.p, b_width, rows, b_width, 64, 64);
   p.blo = ws->split ? tmap_bf16(b.p + b.lo, b_width, rows, b_width, 64, 64) : p.b;
   p.a_split_tiles = a_split_tiles;
@@ -246,8 +251,9 @@ static void wgrad(xmgn_workspace* ws, const BfBuf& a0, const BfBuf& a1, int a_wi
   p.rows = (int)rows;
   p.Hin = Hin;
   p.Hout = H;
+  p.ones_tile = bias_dst >= 0;
   const int NT = H >= 256 ? 256 : H;
-  const int tiles = (Hin / 128) * (H / NT);
+  const int tiles = (Hin / 128 + (p.ones_tile ? 1 : 0)) * (H / NT);
   const int chunks = (int)((rows + 63) / 64);
   int S = (2 * ws->sms + tiles - 1) / tiles;
   if (S > chunks) S = chunks;
@@ -255,21 +261,28 @@ static void wgrad(xmgn_workspace* ws, const BfBuf& a0, const BfBuf& a1, int a_wi
   if (S < 1) S = 1;
   p.n_split = S;
   p.part = ws->part;
-  ProfScope ps("wgrad", st);
-  launch_wgrad(p, ws->split, ws->f16, st);
+  {
+    ProfScope ps("wgrad", st);
+    launch_wgrad(p, ws->split, ws->f16, st);
+  }
   XMGN_CUDA(cudaGetLastError(), "wgrad launch");
-  launch_reduce_part(ws->part, S, (long long)Hin * H, grad + dst, st);
+  const long long ld = (long long)(Hin + (p.ones_tile ? 128 : 0)) * H;
+  if (Hin > 0) launch_reduce_part(ws->part, S, (long long)Hin * H, ld, grad + dst, st);
+  if (p.ones_tile) launch_reduce_part(ws->part + (long long)Hin * H, S, H, ld, grad + bias_dst, st);
 }
 
-static void colsum_reduce(xmgn_workspace* ws, int blk, int l, float* grad, int grid_used, cudaStream_t st) {
+static void colsum_reduce(xmgn_workspace* ws, int blk, int l, float* grad, int grid_used, cudaStream_t st,
+                          bool gamma_only = false) {
   Layout Ly{ws->H, ws->L, ws->m};
   ColsumDst d;
   for (int v = 0; v < NV_MAX; ++v) d.off[v] = -1;
   d.off[0] = Ly.gamma(l, blk);
-  d.off[1] = Ly.beta(l, blk);
-  d.off[2] = Ly.b(l, blk, ws->m);
-  d.off[3] = Ly.b(l, blk, ws->m - 1);
-  if (ws->m >= 2) d.off[4] = Ly.b(l, blk, ws->m - 2);
+  if (!gamma_only) {
+    d.off[1] = Ly.beta(l, blk);
+    d.off[2] = Ly.b(l, blk, ws->m);
+    d.off[3] = Ly.b(l, blk, ws->m - 1);
+    if (ws->m >= 2) d.off[4] = Ly.b(l, blk, ws->m - 2);
+  }
   launch_reduce_colsum(ws->colsum, grid_used, NV_MAX, ws->H, d, grad, st);
 }
 
@@ -345,14 +358,15 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
       ws->a_ck = bfalloc(ws, (size_t)L * NH);
       for (int i = 0; i < 2; ++i) ws->h_buf[i] = (float*)dalloc(ws, NH * 4);
       ws->P = bfalloc(ws, 2 * NH);
-      ws->Ge = bfalloc(ws, EH);
+      ws->Ge[0] = bfalloc(ws, EH);
+      ws->Ge[1] = bfalloc(ws, EH);
       ws->Gh = (float*)dalloc(ws, NH * 4);
       ws->Ga = bfalloc(ws, NH);
       for (int j = 0; j < m; ++j) { ws->scrA[j] = bfalloc(ws, RH); ws->scrS[j] = bfalloc(ws, RH); }
       for (int j = 0; j <= m; ++j) ws->scrZ[j] = bfalloc(ws, RH);
       ws->D = bfalloc(ws, 2 * NH);
       ws->part_splits = 64;
-      ws->part = (float*)dalloc(ws, (size_t)ws->part_splits * 2 * H * H * 4);
+      ws->part = (float*)dalloc(ws, (size_t)ws->part_splits * (2 * H + 128) * H * 4);
       ws->colsum = (float*)dalloc(ws, (size_t)ws->sms * 4 * NV_MAX * H * 4);
       ws->d_flag = (int*)dalloc(ws, 4);
     } catch (...) {
@@ -501,6 +515,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
     XMGN_CUDA(cudaMemcpyAsync(ws->Gh, grad_h_out, P.n_owned * H * sizeof(float), cudaMemcpyDeviceToDevice, st),
               "seed copy");
     const BfBuf none{};
+    int gc = 0;   // which G_e buffer holds G_e^l
     for (int l = L; l >= 1; --l) {
       const int li = l - 1;
       const int64_t nl = n_at(P, L, l), el = e_at(P, L, l), nprev = n_at(P, L, l - 1);
@@ -525,18 +540,19 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         Step& s = pr.add();
         s.a_src = A_ACT; s.K = H; s.b_map = W1; s.b_row0 = r1(li, (blk ? sl_njt(m) : SL_EJT) + m - 1);
         s.epi = EPI_LN_BWD; s.bias = params + Ly.b(li, blk, m);
+        if (blk == 1) s.flags |= EF_COLSUM_ALL;
         s.gamma = params + Ly.gamma(li, blk); s.beta = params + Ly.beta(li, blk);
         s.f_in = ws->Gh; s.ld_in = H;
         s.valid_in = blk ? (int)nl : (int)enext;
         if (blk == 0) {
           s.flags |= EF_G16;
-          s.g16 = ws->Ge.p; s.g16_lo = ws->Ge.lo; s.ga16 = ws->Ga.p; s.ga16_lo = ws->Ga.lo;
+          s.g16 = ws->Ge[gc].p; s.g16_lo = ws->Ge[gc].lo; s.ga16 = ws->Ga.p; s.ga16_lo = ws->Ga.lo;
         }
         s.scr_z = ws->scrZ[m].p; s.lo_off = ws->scrZ[m].lo;
         for (int j = m; j >= 1; --j) {
           Step& d = pr.add();
           d.a_src = A_ACT; d.K = H; d.b_map = W1; d.b_row0 = r1(li, (blk ? sl_nj(m) : sl_ej(m)) + j - 1);
-          d.epi = EPI_DSILU; d.scr_s = ws->scrS[j - 1].p; d.scr_z = ws->scrZ[j - 1].p; d.lo_off = ws->scrZ[j - 1].lo;
+          d.epi = EPI_DSILU; d.flags = blk == 1 ? EF_COLSUM_ALL : 0; d.scr_s = ws->scrS[j - 1].p; d.scr_z = ws->scrZ[j - 1].p; d.lo_off = ws->scrZ[j - 1].lo;
           d.vec0 = 3 + (m - j);
         }
       };
@@ -575,12 +591,17 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         mlp_bwd(pr, 0);
         Step& a = pr.add();   // G_e^{l-1} = G_e' + dZ0 W0[e rows]^T
         a.a_src = A_ACT; a.K = H; a.b_map = W1; a.b_row0 = r1(li, sl_e1e(m));
-        a.epi = EPI_ADD; a.flags = EF_G16; a.g16 = ws->Ge.p; a.g16_lo = ws->Ge.lo;
+        a.epi = EPI_ADD; a.flags = EF_G16; a.g16 = ws->Ge[gc].p; a.g16_lo = ws->Ge[gc].lo;
+        a.g16_out = ws->Ge[gc ^ 1].p;
         run_prog(ws, "chain_edge_bwd", pr, (int)el, dp.src, dp.dst, true, st);
-        colsum_reduce(ws, 0, li, grad_params, chain_grid(ws, (int)el), st);
-        wgrad(ws, eck, none, H, H / 128, ws->scrZ[0], H, 0, el, H, grad_params, Ly.W(li, 0, 0), st);
+        colsum_reduce(ws, 0, li, grad_params, chain_grid(ws, (int)el), st, /*gamma_only=*/true);
+        // bias gradients ride on the weight-gradient GEMMs (all-ones A tile); dbeta = sum_rows G_e'
+        wgrad(ws, eck, none, H, H / 128, ws->scrZ[0], H, 0, el, H, grad_params, Ly.W(li, 0, 0), st, Ly.b(li, 0, 0));
         for (int j = 1; j <= m; ++j)
-          wgrad(ws, ws->scrA[j - 1], none, H, H / 128, ws->scrZ[j], H, 0, el, H, grad_params, Ly.W(li, 0, j), st);
+          wgrad(ws, ws->scrA[j - 1], none, H, H / 128, ws->scrZ[j], H, 0, el, H, grad_params, Ly.W(li, 0, j), st,
+                Ly.b(li, 0, j));
+        wgrad(ws, none, none, H, 0, ws->Ge[gc], H, 0, el, 0, grad_params, 0, st, Ly.beta(li, 0));
+        gc ^= 1;   // G_e^{l-1} now lives in the other buffer
       }
       // D = [sum over out-edges | sum over in-edges] of dZ0 (adjoint of the P gathers)
       { ProfScope ps("segsum", st);
@@ -605,7 +626,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         XMGN_CUDA(cudaMemsetAsync(grad_h0 + n0 * H, 0, (P.n_local - n0) * H * sizeof(float), st), "grad_h0");
     }
     if (grad_e0) {
-      launch_to_f32(ws->f16, ws->Ge.p, ws->Ge.lo, grad_e0, e1 * H, st);
+      launch_to_f32(ws->f16, ws->Ge[gc].p, ws->Ge[gc].lo, grad_e0, e1 * H, st);
       if (P.e_local > e1)
         XMGN_CUDA(cudaMemsetAsync(grad_e0 + e1 * H, 0, (P.e_local - e1) * H * sizeof(float), st), "grad_e0");
     }
