@@ -105,6 +105,7 @@ struct ChainParams {
   const int* dst;     // [M] destination local id
   float* colsum;      // [gridDim.x][4][NV_MAX][H] partial column sums (backward)
   float eps;          // LayerNorm epsilon
+  unsigned long long* trace;  // debug: per-step clock64 stamps of CTA 0 (nullptr = off)
 };
 
 template <int H, bool SPLIT>
@@ -185,26 +186,30 @@ __device__ __forceinline__ void store_tile32(uint8_t* tile, uint32_t lo_off, int
 template <bool SPLIT, bool F16>
 __device__ __forceinline__ void store_bf32(__nv_bfloat16* p, long long lo_off, const float* v) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint32_t hi[4], lo[4];
+  for (int q = 0; q < 2; ++q) {
+    uint32_t hi[8], lo[8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) split2<F16, SPLIT>(v[q * 8 + 2 * i], v[q * 8 + 2 * i + 1], hi[i], lo[i]);
-    reinterpret_cast<uint4*>(p)[q] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    if constexpr (SPLIT) reinterpret_cast<uint4*>(p + lo_off)[q] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    for (int i = 0; i < 8; ++i) split2<F16, SPLIT>(v[q * 16 + 2 * i], v[q * 16 + 2 * i + 1], hi[i], lo[i]);
+    stg256(p + 16 * q, hi);
+    if constexpr (SPLIT) stg256(p + lo_off + 16 * q, lo);
   }
 }
 template <bool SPLIT, bool F16>
 __device__ __forceinline__ void load_bf32(const __nv_bfloat16* p, long long lo_off, float* v) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint4 u = reinterpret_cast<const uint4*>(p)[q];
-    unpack8<F16>(u, v + q * 8);
+  for (int q = 0; q < 2; ++q) {
+    uint32_t u[8];
+    ldg256(p + 16 * q, u);
+    unpack8<F16>(make_uint4(u[0], u[1], u[2], u[3]), v + q * 16);
+    unpack8<F16>(make_uint4(u[4], u[5], u[6], u[7]), v + q * 16 + 8);
     if constexpr (SPLIT) {
-      uint4 w = reinterpret_cast<const uint4*>(p + lo_off)[q];
-      float t[8];
-      unpack8<false>(w, t);
+      uint32_t w[8];
+      ldg256(p + lo_off + 16 * q, w);
+      float t[16];
+      unpack8<false>(make_uint4(w[0], w[1], w[2], w[3]), t);
+      unpack8<false>(make_uint4(w[4], w[5], w[6], w[7]), t + 8);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[q * 8 + i] += t[i];
+      for (int i = 0; i < 16; ++i) v[q * 16 + i] += t[i];
     }
   }
 }
@@ -231,22 +236,15 @@ __device__ __forceinline__ void load_bf32_regs(float* v) {
 }
 __device__ __forceinline__ void load_f32x32(const float* p, float* v) {
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    float4 t = reinterpret_cast<const float4*>(p)[q];
-    v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
-  }
+  for (int q = 0; q < 4; ++q) ldg256(p + 8 * q, reinterpret_cast<uint32_t*>(v + 8 * q));
 }
 __device__ __forceinline__ void load_f32x32_ro(const float* p, float* v) {
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    float4 t = __ldg(reinterpret_cast<const float4*>(p) + q);
-    v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
-  }
+  for (int q = 0; q < 4; ++q) ldg256_nc(p + 8 * q, reinterpret_cast<uint32_t*>(v + 8 * q));
 }
 __device__ __forceinline__ void store_f32x32(float* p, const float* v) {
 #pragma unroll
-  for (int q = 0; q < 8; ++q)
-    reinterpret_cast<float4*>(p)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  for (int q = 0; q < 4; ++q) stg256(p + 8 * q, reinterpret_cast<const uint32_t*>(v + 8 * q));
 }
 
 // Column sums of 32 values over the 32 lanes of a warp: afterwards lane l
@@ -344,6 +342,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
           const bool tma_a = st.a_src == A_TMA;
           if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) { mbar_wait(act_free, naf & 1); ++naf; }
           for (int kc = 0; kc < st.K / 64; ++kc) {
+            if (kc == 1 && p.trace && blockIdx.x == 0 && g < 64) p.trace[g * 8 + 7] = clock64();
             if (tma_a) {
               const int slot = ai % C::SA;
               if (ai >= C::SA) mbar_wait(&a_empty[slot], ((ai / C::SA) - 1) & 1);
@@ -395,6 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
           if (g > 0) mbar_wait(acc_empty, (g - 1) & 1);
           if (st.ctl & CTL_WAIT_ACT) { mbar_wait(act_full, nact & 1); ++nact; }
           tc_fence_after();
+          if (p.trace && blockIdx.x == 0 && g < 64 && lane_id() == 0) p.trace[g * 8 + 0] = clock64();
           for (int kc = 0; kc < st.K / 64; ++kc) {
             int aslot = 0;
             uint32_t a_base;
@@ -439,6 +439,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
           }
           if (elect_one()) mma_commit_cg2_mc(acc_full, 3);
           __syncwarp();
+          if (p.trace && blockIdx.x == 0 && g < 64 && lane_id() == 0) p.trace[g * 8 + 1] = clock64();
         }
       }
     }
@@ -464,13 +465,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
         return t;
       }
     };
-    float colacc[BWD ? NV_MAX : 1][BWD ? NC : 1];
-    if constexpr (BWD) {
-#pragma unroll
-      for (int a = 0; a < NV_MAX; ++a)
-#pragma unroll
-        for (int b = 0; b < NC; ++b) colacc[a][b] = 0.f;
-    }
+    // per-(CTA, quadrant) column-sum partials live in global memory (zeroed by the
+    // host); lane l of this warp owns column c0 + l of every chunk, so the
+    // read-modify-write below is race-free and runs in a fixed order.
+    float* colsum_base = p.colsum ? p.colsum + ((size_t)blockIdx.x * 4 + q) * NV_MAX * H : nullptr;
+    auto colsum_add = [&](int vec, int c0, float* vals) {
+      const float cs = warp_colsum32(vals);
+      float* dstp = colsum_base + (size_t)vec * H + c0 + lane;
+      *dstp += cs;
+    };
     const uint32_t acc_empty_l = mapa_shared(smem_u32(acc_empty), 0);
     const uint32_t act_full_l = mapa_shared(smem_u32(act_full), 0);
     int g = 0;
@@ -484,6 +487,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
         const Step& st = p.steps[s];
         mbar_wait(acc_full, g & 1);
         tc_fence_after();
+        if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 2] = clock64();
         bool wrote_act = false;
         float v[32], pb[32];
         if (st.epi == EPI_SILU) {
@@ -538,6 +542,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
             for (int i = 0; i < 32; ++i) { float d = v[i] + pb[i] - mean; sq += d * d; }
           }
           const float rstd = rsqrtf(row_sum(sq) * (1.0f / H) + p.eps);
+          if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 3] = clock64();
           if (st.epi == EPI_LN_FWD) {
 #pragma unroll 1
             for (int cc = 0; cc < NC; ++cc) {
@@ -569,7 +574,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
             // LayerNorm backward: dx^ = dY*gamma; dz = rstd (dx^ - mean(dx^) - x^ mean(dx^ x^))
             const bool has_g = valid && r < st.valid_in;
             float s1 = 0.f, s2 = 0.f;
-#pragma unroll
+#pragma unroll 1
             for (int cc = 0; cc < NC; ++cc) {
               const int c0 = cb + cc * 32;
               tmem_ld32(tl + cc * 32, v);
@@ -605,12 +610,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
                 t1[i] = valid ? dy[i] * xh : 0.f;
                 t2[i] = valid ? dy[i] : 0.f;
               }
-              colacc[0][cc] += warp_colsum32(t1);   // dgamma
-              if (st.flags & EF_COLSUM_ALL) colacc[1][cc] += warp_colsum32(t2);   // dbeta
+              colsum_add(0, c0, t1);                               // dgamma
+              if (st.flags & EF_COLSUM_ALL) colsum_add(1, c0, t2);  // dbeta
             }
             s1 = row_sum(s1) * (1.0f / H);
             s2 = row_sum(s2) * (1.0f / H);
-#pragma unroll
+            if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 4] = clock64();
+#pragma unroll 1
             for (int cc = 0; cc < NC; ++cc) {
               const int c0 = cb + cc * 32;
               tmem_ld32(tl + cc * 32, v);
@@ -634,13 +640,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
               }
               store_tile32<H, SPLIT, F16>(act, C::ACT_HALF, trow, c0, v);
               if (valid) store_bf32<SPLIT, F16>(st.scr_z + (size_t)r * H + c0, st.lo_off, v);
-              if (st.flags & EF_COLSUM_ALL) colacc[2][cc] += warp_colsum32(v);    // db_{m+1}
+              if (st.flags & EF_COLSUM_ALL) colsum_add(2, c0, v);   // db_{m+1}
             }
             wrote_act = true;
           }
         } else if (st.epi == EPI_DSILU) {
           if constexpr (BWD) {
-#pragma unroll
+#pragma unroll 1
             for (int cc = 0; cc < NC; ++cc) {
               const int c0 = cb + cc * 32;
               tmem_ld32(tl + cc * 32, v);
@@ -650,11 +656,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
               for (int i = 0; i < 32; ++i) v[i] = valid ? v[i] * sd[i] : 0.f;
               store_tile32<H, SPLIT, F16>(act, C::ACT_HALF, trow, c0, v);
               if (valid) store_bf32<SPLIT, F16>(st.scr_z + (size_t)r * H + c0, st.lo_off, v);
-              if (st.flags & EF_COLSUM_ALL) {
-                const float cs = warp_colsum32(v);
-                if (st.vec0 == 3) colacc[3][cc] += cs;  // db_m
-                else colacc[4][cc] += cs;               // db_{m-1}
-              }
+              if (st.flags & EF_COLSUM_ALL) colsum_add(st.vec0, c0, v);  // db_m (3) / db_{m-1} (4)
             }
             wrote_act = true;
           }
@@ -707,19 +709,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
         tc_fence_before();
         if (wrote_act) fence_proxy_async_smem();
         __syncwarp();
+        if (p.trace && blockIdx.x == 0 && g < 64 && lane == 0 && (w == 4 || w == 8)) p.trace[g * 8 + (w == 4 ? 5 : 6)] = clock64();
         if (lane == 0) {
           mbar_arrive_cluster(acc_empty_l);
           if (wrote_act) mbar_arrive_cluster(act_full_l);
         }
-      }
-    }
-    if constexpr (BWD) {
-      if (p.colsum) {
-        float* out = p.colsum + ((size_t)blockIdx.x * 4 + q) * NV_MAX * H + cb;
-#pragma unroll
-        for (int a = 0; a < NV_MAX; ++a)
-#pragma unroll
-          for (int b = 0; b < NC; ++b) out[a * H + b * 32 + lane] = colacc[a][b];
       }
     }
   }

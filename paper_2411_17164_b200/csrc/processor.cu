@@ -13,6 +13,8 @@
 // updates destinations of ring <= L-l, a prefix of nodes (n_l) and of edges
 // (E_l); the skipped rows feed only discarded halo outputs.
 #include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #include "graph.h"
@@ -210,8 +212,40 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
   const int pair_tiles = (M + 255) / 256;
   const int grid = 2 * (pair_tiles < ws->sms / 2 ? pair_tiles : ws->sms / 2);
   p.colsum = bwd ? ws->colsum : nullptr;
-  ProfScope ps(name, st);
-  launch_chain(ws->H, ws->split, ws->f16, bwd, p, grid, st);
+  if (bwd)
+    XMGN_CUDA(cudaMemsetAsync(ws->colsum, 0, (size_t)grid * 4 * NV_MAX * ws->H * sizeof(float), st), "colsum zero");
+  // debug tracing (XMGN_TRACE=<scope name>): clock64 stamps of CTA 0, first launch only
+  static unsigned long long* trace_buf = nullptr;
+  static bool traced = false;
+  const char* tr = getenv("XMGN_TRACE");
+  const bool do_trace = tr && !traced && strcmp(tr, name) == 0;
+  if (do_trace) {
+    cudaMalloc(&trace_buf, 64 * 8 * 8);
+    cudaMemsetAsync(trace_buf, 0, 64 * 8 * 8, st);
+    p.trace = trace_buf;
+  }
+  {
+    ProfScope ps(name, st);
+    launch_chain(ws->H, ws->split, ws->f16, bwd, p, grid, st);
+  }
+  if (do_trace) {
+    traced = true;
+    unsigned long long h[64 * 8];
+    cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    FILE* f = fopen("gpurun_out/trace.txt", "w");
+    if (f) {
+      fprintf(f, "# %s M=%d steps=%d: g, mma_start, mma_issued, epi_start, ln_stats, lnbwd_passA, epi_end_w4, epi_end_w8, prod_kc1\n",
+              name, M, pr.n);
+      const unsigned long long t0 = h[0];
+      for (int g = 0; g < 64; ++g) {
+        fprintf(f, "%d", g);
+        for (int k = 0; k < 8; ++k) fprintf(f, " %lld", h[g * 8 + k] ? (long long)(h[g * 8 + k] - t0) : -1LL);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+  }
   XMGN_CUDA(cudaGetLastError(), "chain kernel launch");
 }
 
