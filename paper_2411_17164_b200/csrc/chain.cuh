@@ -121,7 +121,7 @@ struct ChainCfg {
   static constexpr uint32_t B_SLOT_HALF = NBH * 128u;
   static constexpr uint32_t B_SLOT = F * B_SLOT_HALF;
   static constexpr uint32_t SMEM_LIMIT = 227u * 1024u;
-  static constexpr int SB_FIT = (int)((SMEM_LIMIT - 2560u - ACT_BYTES) / B_SLOT);
+  static constexpr int SB_FIT = (int)((SMEM_LIMIT - 1536u - 512u * EPI_GROUPS - ACT_BYTES) / B_SLOT);
   static constexpr int SB = SB_FIT > 8 ? 8 : SB_FIT;
   static constexpr uint32_t BAR_OFF = ACT_BYTES + SB * B_SLOT;
   static constexpr uint32_t RED_OFF = BAR_OFF + 512;             // row-reduction exchange [EW][128] f32
@@ -523,25 +523,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
           }
           wrote_act = true;
         } else if (st.epi == EPI_LN_FWD || st.epi == EPI_LN_BWD) {
-          // z = acc + b; two-pass mean / variance over the H columns of this row
-          float sum = 0.f;
+          // z = acc + b; mean and variance over the H columns of this row in one TMEM pass
+          // (sum and sum of squares in FP32; var = E[z^2] - mean^2, clamped at 0)
+          float sum = 0.f, sq = 0.f;
 #pragma unroll 1
           for (int cc = 0; cc < NC; ++cc) {
             tmem_ld32(tl + cc * 32, v);
             load_f32x32_ro(st.bias + cb + cc * 32, pb);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) sum += v[i] + pb[i];
+            for (int i = 0; i < 32; ++i) { const float z = v[i] + pb[i]; sum += z; sq = fmaf(z, z, sq); }
           }
           const float mean = row_sum(sum) * (1.0f / H);
-          float sq = 0.f;
-#pragma unroll 1
-          for (int cc = 0; cc < NC; ++cc) {
-            tmem_ld32(tl + cc * 32, v);
-            load_f32x32_ro(st.bias + cb + cc * 32, pb);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) { float d = v[i] + pb[i] - mean; sq += d * d; }
-          }
-          const float rstd = rsqrtf(row_sum(sq) * (1.0f / H) + p.eps);
+          const float var = fmaxf(row_sum(sq) * (1.0f / H) - mean * mean, 0.f);
+          const float rstd = rsqrtf(var + p.eps);
           if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 3] = clock64();
           if (st.epi == EPI_LN_FWD) {
 #pragma unroll 1
@@ -646,12 +640,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
           }
         } else if (st.epi == EPI_DSILU) {
           if constexpr (BWD) {
+            // S' rows are software-pipelined one chunk ahead (raw 16-bit registers)
+            uint32_t cur[16], nxt[16];
+            const __nv_bfloat16* srow = st.scr_s + (size_t)r * H + cb;
+            if (!SPLIT && valid) { ldg256(srow, cur); ldg256(srow + 16, cur + 8); }
 #pragma unroll 1
             for (int cc = 0; cc < NC; ++cc) {
               const int c0 = cb + cc * 32;
+              if (!SPLIT && valid && cc + 1 < NC) {
+                ldg256(srow + (cc + 1) * 32, nxt);
+                ldg256(srow + (cc + 1) * 32 + 16, nxt + 8);
+              }
               tmem_ld32(tl + cc * 32, v);
               float sd[32];
-              if (valid) load_bf32<SPLIT, F16>(st.scr_s + (size_t)r * H + c0, st.lo_off, sd);
+              if constexpr (SPLIT) {
+                if (valid) load_bf32<SPLIT, F16>(st.scr_s + (size_t)r * H + c0, st.lo_off, sd);
+              } else {
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4)
+                  unpack8<F16>(make_uint4(cur[4 * q4], cur[4 * q4 + 1], cur[4 * q4 + 2], cur[4 * q4 + 3]), sd + 8 * q4);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+              }
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = valid ? v[i] * sd[i] : 0.f;
               store_tile32<H, SPLIT, F16>(act, C::ACT_HALF, trow, c0, v);
