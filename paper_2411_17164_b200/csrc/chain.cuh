@@ -121,11 +121,13 @@ struct ChainCfg {
   static constexpr uint32_t B_SLOT_HALF = NBH * 128u;
   static constexpr uint32_t B_SLOT = F * B_SLOT_HALF;
   static constexpr uint32_t SMEM_LIMIT = 227u * 1024u;
-  static constexpr int SB_FIT = (int)((SMEM_LIMIT - 1536u - 512u * EPI_GROUPS - ACT_BYTES) / B_SLOT);
+  static constexpr uint32_t PRM_BYTES = 2u * 3u * H * 4u;        // per-step bias/gamma/beta, double-buffered
+  static constexpr int SB_FIT = (int)((SMEM_LIMIT - 1536u - 512u * EPI_GROUPS - PRM_BYTES - ACT_BYTES) / B_SLOT);
   static constexpr int SB = SB_FIT > 8 ? 8 : SB_FIT;
   static constexpr uint32_t BAR_OFF = ACT_BYTES + SB * B_SLOT;
   static constexpr uint32_t RED_OFF = BAR_OFF + 512;             // row-reduction exchange [EW][128] f32
-  static constexpr uint32_t SMEM_BYTES = RED_OFF + EPI_GROUPS * 128 * 4 + 1024;  // + alignment slack
+  static constexpr uint32_t PRM_OFF = RED_OFF + EPI_GROUPS * 128 * 4;
+  static constexpr uint32_t SMEM_BYTES = PRM_OFF + PRM_BYTES + 1024;  // + alignment slack
   static constexpr uint32_t TMEM_COLS = H;
   static_assert(SB >= 2, "B ring too small");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
@@ -264,6 +266,88 @@ __device__ __forceinline__ float warp_colsum32(float* v) {
   return v[0];
 }
 
+// ---- helpers of the pipelined 16-bit epilogue
+__device__ __forceinline__ void ld16x32(const __nv_bfloat16* p, uint32_t* r) {  // 32 x 16-bit (64 B)
+  ldg256(p, r);
+  ldg256(p + 16, r + 8);
+}
+template <bool F16>
+__device__ __forceinline__ void cvt16x32(const uint32_t* r, float* v) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) unpack8<F16>(make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]), v + 8 * q);
+}
+template <bool F16>
+__device__ __forceinline__ void add16x32(const uint32_t* r, float* v) {
+  float t[32];
+  cvt16x32<F16>(r, t);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] += t[i];
+}
+template <bool F16>
+__device__ __forceinline__ void st16x32(__nv_bfloat16* p, const float* v) {
+  uint32_t h[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) h[i] = pack16<F16>(v[2 * i], v[2 * i + 1]);
+  stg256(p, h);
+  stg256(p + 16, h + 8);
+}
+template <bool F16>
+__device__ __forceinline__ void round16x32(float* v) {
+  uint32_t h[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) h[i] = pack16<F16>(v[2 * i], v[2 * i + 1]);
+  cvt16x32<F16>(h, v);
+}
+__device__ __forceinline__ void lds_f32x32(const float* p, float* v) {  // broadcast read
+  const uint32_t a = smem_u32(p);
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v[4 * q]), "=f"(v[4 * q + 1]), "=f"(v[4 * q + 2]), "=f"(v[4 * q + 3])
+                 : "r"(a + 16 * q));
+}
+// SiLU(x) = h + h tanh(h), h = x/2.  FP16 mode: tanh on packed f16x2 (one MUFU op per
+// two elements; its ~2^-11 error is at the FP16 rounding of the stored activation).
+template <bool F16>
+__device__ __forceinline__ void tanh2(float a, float b, float& ta, float& tb) {
+  if constexpr (F16) {
+    uint32_t hh = pack16<true>(a, b), tt;
+    asm("tanh.approx.f16x2 %0, %1;" : "=r"(tt) : "r"(hh));
+    const __half2 t2 = *reinterpret_cast<const __half2*>(&tt);
+    ta = __low2float(t2);
+    tb = __high2float(t2);
+  } else {
+    asm("tanh.approx.f32 %0, %1;" : "=f"(ta) : "f"(a));
+    asm("tanh.approx.f32 %0, %1;" : "=f"(tb) : "f"(b));
+  }
+}
+template <bool F16>
+__device__ __forceinline__ void silu32(float* x) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {
+    const float ha = 0.5f * x[i], hb = 0.5f * x[i + 1];
+    float ta, tb;
+    tanh2<F16>(ha, hb, ta, tb);
+    x[i] = fmaf(ha, ta, ha);
+    x[i + 1] = fmaf(hb, tb, hb);
+  }
+}
+// x <- SiLU(x), d <- SiLU'(x) = s + x s (1 - s), s = (1 + tanh(x/2)) / 2
+template <bool F16>
+__device__ __forceinline__ void silu_grad32(float* x, float* d) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {
+    const float ha = 0.5f * x[i], hb = 0.5f * x[i + 1];
+    float ta, tb;
+    tanh2<F16>(ha, hb, ta, tb);
+    const float sa = fmaf(0.5f, ta, 0.5f), sb2 = fmaf(0.5f, tb, 0.5f);
+    d[i] = fmaf(x[i] * sa, 1.0f - sa, sa);
+    d[i + 1] = fmaf(x[i + 1] * sb2, 1.0f - sb2, sb2);
+    x[i] = fmaf(ha, ta, ha);
+    x[i + 1] = fmaf(hb, tb, hb);
+  }
+}
+
 // dY of the LayerNorm backward: incoming gradient rows (< valid_in) plus the
 // aggregation adjoint G_a[dst] for edge programs.
 __device__ __forceinline__ void load_dy(const Step& st, bool has_g, bool valid, int r, int dst, int c0, float* dy) {
@@ -306,6 +390,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
   uint64_t* mma_idle = act_free + 1;         // MMA -> itself (all issued MMAs retired)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(mma_idle + 1);
   float* red = reinterpret_cast<float*>(smem + C::RED_OFF);
+  float* prm_base = reinterpret_cast<float*>(smem + C::PRM_OFF);
 
   const int w = warp_id();
   const uint32_t rank = cluster_ctarank();
@@ -331,6 +416,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
+  // register split (setmaxnreg, per warpgroup): control warps 0-3 need few registers,
+  // the epilogue warpgroups get the rest
+  if (w < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
   if (w == 0) {
     // ============================ TMA producer (both CTAs: own A rows, own half of B)
     if (elect_one()) {
@@ -443,7 +532,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
         }
       }
     }
-  } else if (w >= 4) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
     // ============================ epilogue: thread = tile row (TMEM lane) x HC columns
     const int q = w & 3;                 // TMEM lane quadrant
     const int eg = (w - 4) >> 2;         // column group
@@ -485,12 +576,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
       const int dst = p.dst ? p.dst[rr] : 0;
       for (int s = 0; s < p.n_steps; ++s, ++g) {
         const Step& st = p.steps[s];
+        float* prm = prm_base + (g & 1) * 3 * H;
+        if constexpr (!SPLIT) {
+          // stage this step's bias / gamma / beta into shared memory while the MMAs run
+          const int et = threadIdx.x - 128;
+          for (int i = et; i < 3 * H; i += NEPI) {
+            const float* srcv = i < H ? st.bias : (i < 2 * H ? st.gamma : st.beta);
+            prm[i] = srcv ? __ldg(srcv + (i % H)) : 0.f;
+          }
+          named_bar(7, NEPI);
+        }
         mbar_wait(acc_full, g & 1);
         tc_fence_after();
         if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 2] = clock64();
         bool wrote_act = false;
+        if constexpr (SPLIT) {
         float v[32], pb[32];
-        if (st.epi == EPI_SILU) {
+        if (st.epi == EPI_SILU && !(st.flags & (EF_GATHER_P | EF_STORE_S | EF_STORE_A))) {
+          // plain SiLU epilogue, software-pipelined one chunk ahead (TMEM + bias)
+          uint32_t ta[32];
+          float bn[32];
+          tmem_ld32_async(tl, ta);
+          load_f32x32_ro(st.bias + cb, bn);
+#pragma unroll 1
+          for (int cc = 0; cc < NC; ++cc) {
+            const int c0 = cb + cc * 32;
+            tmem_wait32(ta);
+            float x[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(ta[i]) + bn[i];
+            if (cc + 1 < NC) {
+              tmem_ld32_async(tl + (cc + 1) * 32, ta);
+              load_f32x32_ro(st.bias + c0 + 32, bn);
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = silu_<SPLIT>(x[i]);
+            store_tile32<H, SPLIT, F16>(act, C::ACT_HALF, trow, c0, x);
+          }
+          wrote_act = true;
+        } else if (st.epi == EPI_SILU) {
 #pragma unroll 1
           for (int cc = 0; cc < NC; ++cc) {
             const int c0 = cb + cc * 32;
@@ -713,6 +837,286 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
                 for (int i = 0; i < 32; ++i) v[i] += t[i];
               }
               store_f32x32(st.f_out + (size_t)r * st.ld_out + c0, v);
+            }
+          }
+        }
+        } else {
+          // ---------------- software-pipelined epilogue (16-bit operand modes)
+          // per-step parameter vectors live in shared memory (staged above)
+          const float* sb = prm + cb;            // bias
+          const float* sg = prm + H + cb;        // gamma
+          const float* sbt = prm + 2 * H + cb;   // beta
+          uint32_t ta[32];
+          const int op = st.epi;
+          if (op == EPI_SILU) {
+            const bool gp = (st.flags & EF_GATHER_P) != 0;
+            const bool sa = (st.flags & EF_STORE_A) != 0, ss = (st.flags & EF_STORE_S) != 0;
+            const __nv_bfloat16* ps = st.gather16 + (size_t)src * 2 * H + cb;
+            const __nv_bfloat16* pd = st.gather16 + (size_t)dst * 2 * H + H + cb;
+            uint32_t gs[16], gd[16];
+            tmem_ld32_async(tl, ta);
+            if (gp) { ld16x32(ps, gs); ld16x32(pd, gd); }
+#pragma unroll 1
+            for (int cc = 0; cc < NC; ++cc) {
+              const int c0 = cb + cc * 32;
+              float x[32];
+              lds_f32x32(sb + cc * 32, x);
+              if (gp) { add16x32<F16>(gs, x); add16x32<F16>(gd, x); }
+              tmem_wait32(ta);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) x[i] += __uint_as_float(ta[i]);
+              if (cc + 1 < NC) {
+                tmem_ld32_async(tl + (cc + 1) * 32, ta);
+                if (gp) { ld16x32(ps + (cc + 1) * 32, gs); ld16x32(pd + (cc + 1) * 32, gd); }
+              }
+              if (ss) {
+                float dv[32];
+                silu_grad32<F16>(x, dv);          // x <- SiLU(x), dv <- SiLU'(x)
+                if (valid) st16x32<F16>(st.scr_s + (size_t)r * H + c0, dv);
+              } else {
+                silu32<F16>(x);
+              }
+              store_tile32<H, false, F16>(act, C::ACT_HALF, trow, c0, x);
+              if (sa && valid) st16x32<F16>(st.scr_a + (size_t)r * H + c0, x);
+            }
+            wrote_act = true;
+          } else if (op == EPI_LN_FWD || op == EPI_LN_BWD) {
+            // one TMEM pass for mean / E[z^2]
+            float sum = 0.f, sq = 0.f;
+            tmem_ld32_async(tl, ta);
+#pragma unroll 1
+            for (int cc = 0; cc < NC; ++cc) {
+              float b[32];
+              lds_f32x32(sb + cc * 32, b);
+              tmem_wait32(ta);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) b[i] += __uint_as_float(ta[i]);
+              if (cc + 1 < NC) tmem_ld32_async(tl + (cc + 1) * 32, ta);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) { sum += b[i]; sq = fmaf(b[i], b[i], sq); }
+            }
+            const float mean = row_sum(sum) * (1.0f / H);
+            const float var = fmaxf(row_sum(sq) * (1.0f / H) - mean * mean, 0.f);
+            const float rstd = rsqrtf(var + p.eps);
+            if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 3] = clock64();
+            if (op == EPI_LN_FWD) {
+              const bool r16 = (st.flags & EF_RES16) != 0;
+              const __nv_bfloat16* rp = st.res16 + (size_t)r * H + cb;
+              uint32_t rr16[16];
+              tmem_ld32_async(tl, ta);
+              if (r16 && valid) ld16x32(rp, rr16);
+#pragma unroll 1
+              for (int cc = 0; cc < NC; ++cc) {
+                const int c0 = cb + cc * 32;
+                float y[32], res[32];
+                if (r16) {
+                  if (valid) cvt16x32<F16>(rr16, res);
+                  else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) res[i] = 0.f;
+                  }
+                } else if (valid) {
+                  load_f32x32(st.f_in + (size_t)r * st.ld_in + c0, res);
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) res[i] = 0.f;
+                }
+                lds_f32x32(sb + cc * 32, y);
+                tmem_wait32(ta);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) y[i] = (y[i] + __uint_as_float(ta[i]) - mean) * rstd;
+                if (cc + 1 < NC) {
+                  tmem_ld32_async(tl + (cc + 1) * 32, ta);
+                  if (r16 && valid) ld16x32(rp + (cc + 1) * 32, rr16);
+                }
+                {
+                  float gm[32];
+                  lds_f32x32(sg + cc * 32, gm);
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) y[i] = fmaf(gm[i], y[i], res[i]);
+                  lds_f32x32(sbt + cc * 32, gm);
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) y[i] += gm[i];
+                }
+                if (valid) {
+                  if (st.flags & EF_STORE_F32) store_f32x32(st.f_out + (size_t)r * st.ld_out + c0, y);
+                  if (st.flags & EF_STORE_BF) st16x32<F16>(st.bf_out + (size_t)r * H + c0, y);
+                }
+                if (st.flags & EF_WRITE_ACT) store_tile32<H, false, F16>(act, C::ACT_HALF, trow, c0, y);
+              }
+              wrote_act = (st.flags & EF_WRITE_ACT) != 0;
+            } else if constexpr (BWD) {
+              // LayerNorm backward (see the SPLIT path for the formula)
+              const bool g16 = (st.flags & EF_G16) != 0;
+              const bool has_g = valid && r < st.valid_in;
+              const __nv_bfloat16* gp16 = st.g16 + (size_t)r * H + cb;
+              const __nv_bfloat16* ap16 = st.ga16 + (size_t)dst * H + cb;
+              uint32_t g1[16], g2[16];
+              float s1 = 0.f, s2 = 0.f;
+              tmem_ld32_async(tl, ta);
+              if (g16) {
+                if (has_g) ld16x32(gp16, g1);
+                if (valid) ld16x32(ap16, g2);
+              }
+#pragma unroll 1
+              for (int cc = 0; cc < NC; ++cc) {
+                const int c0 = cb + cc * 32;
+                float dy[32], xh[32];
+                if (g16) {
+                  if (has_g) cvt16x32<F16>(g1, dy);
+                  else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) dy[i] = 0.f;
+                  }
+                  if (valid) {
+                    add16x32<F16>(g2, dy);
+                    round16x32<F16>(dy);                      // as stored (G_e')
+                    st16x32<F16>(st.g16 + (size_t)r * H + c0, dy);
+                  }
+                } else {
+                  load_dy(st, has_g, valid, r, dst, c0, dy);
+                }
+                lds_f32x32(sb + cc * 32, xh);
+                tmem_wait32(ta);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) xh[i] = (xh[i] + __uint_as_float(ta[i]) - mean) * rstd;
+                if (cc + 1 < NC) {
+                  tmem_ld32_async(tl + (cc + 1) * 32, ta);
+                  if (g16) {
+                    if (has_g) ld16x32(gp16 + (cc + 1) * 32, g1);
+                    if (valid) ld16x32(ap16 + (cc + 1) * 32, g2);
+                  }
+                }
+                float gm[32];
+                lds_f32x32(sg + cc * 32, gm);
+                float t1[32], t2[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const float dxh = dy[i] * gm[i];
+                  s1 += dxh;
+                  s2 += dxh * xh[i];
+                  t1[i] = valid ? dy[i] * xh[i] : 0.f;
+                  t2[i] = valid ? dy[i] : 0.f;
+                }
+                colsum_add(0, c0, t1);                               // dgamma
+                if (st.flags & EF_COLSUM_ALL) colsum_add(1, c0, t2);  // dbeta
+              }
+              s1 = row_sum(s1) * (1.0f / H);
+              s2 = row_sum(s2) * (1.0f / H);
+              if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 4] = clock64();
+              // pass B: dz = rstd (dxh - mean(dxh) - xh mean(dxh xh))
+              tmem_ld32_async(tl, ta);
+              if (g16 && valid) ld16x32(gp16, g1);     // G_e' (written in pass A by this thread)
+#pragma unroll 1
+              for (int cc = 0; cc < NC; ++cc) {
+                const int c0 = cb + cc * 32;
+                float dy[32], xh[32];
+                if (g16) {
+                  if (valid) cvt16x32<F16>(g1, dy);
+                  else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) dy[i] = 0.f;
+                  }
+                } else {
+                  load_dy(st, has_g, valid, r, dst, c0, dy);
+                }
+                lds_f32x32(sb + cc * 32, xh);
+                tmem_wait32(ta);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) xh[i] = (xh[i] + __uint_as_float(ta[i]) - mean) * rstd;
+                if (cc + 1 < NC) {
+                  tmem_ld32_async(tl + (cc + 1) * 32, ta);
+                  if (g16 && valid) ld16x32(gp16 + (cc + 1) * 32, g1);
+                }
+                float gm[32];
+                lds_f32x32(sg + cc * 32, gm);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) dy[i] = valid ? rstd * (dy[i] * gm[i] - s1 - xh[i] * s2) : 0.f;
+                store_tile32<H, false, F16>(act, C::ACT_HALF, trow, c0, dy);
+                if (valid) st16x32<F16>(st.scr_z + (size_t)r * H + c0, dy);
+                if (st.flags & EF_COLSUM_ALL) colsum_add(2, c0, dy);   // db_{m+1}
+              }
+              wrote_act = true;
+            }
+          } else if (op == EPI_DSILU) {
+            if constexpr (BWD) {
+              const __nv_bfloat16* sp = st.scr_s + (size_t)r * H + cb;
+              uint32_t sr[16];
+              tmem_ld32_async(tl, ta);
+              if (valid) ld16x32(sp, sr);
+#pragma unroll 1
+              for (int cc = 0; cc < NC; ++cc) {
+                const int c0 = cb + cc * 32;
+                float x[32];
+                if (valid) cvt16x32<F16>(sr, x);
+                tmem_wait32(ta);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) x[i] = valid ? x[i] * __uint_as_float(ta[i]) : 0.f;
+                if (cc + 1 < NC) {
+                  tmem_ld32_async(tl + (cc + 1) * 32, ta);
+                  if (valid) ld16x32(sp + (cc + 1) * 32, sr);
+                }
+                store_tile32<H, false, F16>(act, C::ACT_HALF, trow, c0, x);
+                if (valid) st16x32<F16>(st.scr_z + (size_t)r * H + c0, x);
+                if (st.flags & EF_COLSUM_ALL) colsum_add(st.vec0, c0, x);
+              }
+              wrote_act = true;
+            }
+          } else if (op == EPI_STORE) {
+            tmem_ld32_async(tl, ta);
+#pragma unroll 1
+            for (int cc = 0; cc < NC; ++cc) {
+              const int c0 = cb + cc * 32;
+              tmem_wait32(ta);
+              float x[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(ta[i]);
+              if (cc + 1 < NC) tmem_ld32_async(tl + (cc + 1) * 32, ta);
+              if (valid) {
+                if (st.flags & EF_OUT16) st16x32<F16>(st.bf_out + (size_t)r * st.ld_out + st.col0 + c0, x);
+                else store_f32x32(st.f_out + (size_t)r * st.ld_out + st.col0 + c0, x);
+              }
+            }
+          } else if (op == EPI_ADD) {
+            const bool g16 = (st.flags & EF_G16) != 0;
+            const bool has_in = valid && r < st.valid_in;
+            const __nv_bfloat16* ip = st.g16 + (size_t)r * H + cb;
+            uint32_t ir[16];
+            tmem_ld32_async(tl, ta);
+            if (g16 && valid) ld16x32(ip, ir);
+#pragma unroll 1
+            for (int cc = 0; cc < NC; ++cc) {
+              const int c0 = cb + cc * 32;
+              float x[32];
+              if (g16) {
+                if (valid) cvt16x32<F16>(ir, x);
+                else {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) x[i] = 0.f;
+                }
+              } else if (has_in) {
+                load_f32x32(st.f_in + (size_t)r * st.ld_in + c0, x);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) x[i] = 0.f;
+              }
+              if (!g16 && valid && (st.flags & EF_GATHER_G)) {
+                float t[32];
+                load_f32x32(st.gather + (size_t)dst * H + c0, t);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) x[i] += t[i];
+              }
+              tmem_wait32(ta);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) x[i] += __uint_as_float(ta[i]);
+              if (cc + 1 < NC) {
+                tmem_ld32_async(tl + (cc + 1) * 32, ta);
+                if (g16 && valid) ld16x32(ip + (cc + 1) * 32, ir);
+              }
+              if (valid) {
+                if (g16) st16x32<F16>(st.g16_out + (size_t)r * H + c0, x);
+                else store_f32x32(st.f_out + (size_t)r * st.ld_out + c0, x);
+              }
             }
           }
         }
