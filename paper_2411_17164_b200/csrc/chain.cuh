@@ -106,6 +106,7 @@ struct ChainParams {
   float* colsum;      // [gridDim.x][4][NV_MAX][H] partial column sums (backward)
   float eps;          // LayerNorm epsilon
   unsigned long long* trace;  // debug: per-step clock64 stamps of CTA 0 (nullptr = off)
+  int dbg;                    // debug experiment bits (0 in production)
 };
 
 template <int H, bool SPLIT>
@@ -842,18 +843,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
         }
         } else {
           // ---------------- software-pipelined epilogue (16-bit operand modes)
-          // per-step parameter vectors live in shared memory (staged above)
+          // Each op: the step's fields are read once into registers, parameter vectors come
+          // from shared memory, and TMEM + 16-bit row inputs are prefetched one 32-column
+          // chunk ahead.  Arrays are defined unconditionally (invalid rows load zeros).
           const float* sb = prm + cb;            // bias
           const float* sg = prm + H + cb;        // gamma
           const float* sbt = prm + 2 * H + cb;   // beta
-          uint32_t ta[32];
           const int op = st.epi;
+          const int fl = st.flags;
+          uint32_t ta[32];
           if (op == EPI_SILU) {
-            const bool gp = (st.flags & EF_GATHER_P) != 0;
-            const bool sa = (st.flags & EF_STORE_A) != 0, ss = (st.flags & EF_STORE_S) != 0;
+            const bool gp = (fl & EF_GATHER_P) != 0;
+            const bool sa = valid && (fl & EF_STORE_A) != 0, ss = (fl & EF_STORE_S) != 0;
             const __nv_bfloat16* ps = st.gather16 + (size_t)src * 2 * H + cb;
             const __nv_bfloat16* pd = st.gather16 + (size_t)dst * 2 * H + H + cb;
+            __nv_bfloat16* oa = st.scr_a + (size_t)r * H + cb;
+            __nv_bfloat16* os = st.scr_s + (size_t)r * H + cb;
             uint32_t gs[16], gd[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) { gs[i] = 0u; gd[i] = 0u; }
             tmem_ld32_async(tl, ta);
             if (gp) { ld16x32(ps, gs); ld16x32(pd, gd); }
 #pragma unroll 1
@@ -861,7 +869,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
               const int c0 = cb + cc * 32;
               float x[32];
               lds_f32x32(sb + cc * 32, x);
-              if (gp) { add16x32<F16>(gs, x); add16x32<F16>(gd, x); }
+              add16x32<F16>(gs, x);
+              add16x32<F16>(gd, x);
               tmem_wait32(ta);
 #pragma unroll
               for (int i = 0; i < 32; ++i) x[i] += __uint_as_float(ta[i]);
@@ -872,12 +881,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
               if (ss) {
                 float dv[32];
                 silu_grad32<F16>(x, dv);          // x <- SiLU(x), dv <- SiLU'(x)
-                if (valid) st16x32<F16>(st.scr_s + (size_t)r * H + c0, dv);
+                if (valid) st16x32<F16>(os + cc * 32, dv);
               } else {
                 silu32<F16>(x);
               }
               store_tile32<H, false, F16>(act, C::ACT_HALF, trow, c0, x);
-              if (sa && valid) st16x32<F16>(st.scr_a + (size_t)r * H + c0, x);
+              if (sa) st16x32<F16>(oa + cc * 32, x);
             }
             wrote_act = true;
           } else if (op == EPI_LN_FWD || op == EPI_LN_BWD) {
@@ -900,26 +909,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
             const float rstd = rsqrtf(var + p.eps);
             if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 3] = clock64();
             if (op == EPI_LN_FWD) {
-              const bool r16 = (st.flags & EF_RES16) != 0;
+              const bool r16 = (fl & EF_RES16) != 0, w32 = valid && (fl & EF_STORE_F32) != 0;
+              const bool w16 = valid && (fl & EF_STORE_BF) != 0, wact = (fl & EF_WRITE_ACT) != 0;
               const __nv_bfloat16* rp = st.res16 + (size_t)r * H + cb;
+              const float* rp32 = st.f_in + (size_t)r * st.ld_in + cb;
+              float* op32 = st.f_out + (size_t)r * st.ld_out + cb;
+              __nv_bfloat16* op16 = st.bf_out + (size_t)r * H + cb;
               uint32_t rr16[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) rr16[i] = 0u;
               tmem_ld32_async(tl, ta);
               if (r16 && valid) ld16x32(rp, rr16);
 #pragma unroll 1
               for (int cc = 0; cc < NC; ++cc) {
                 const int c0 = cb + cc * 32;
                 float y[32], res[32];
-                if (r16) {
-                  if (valid) cvt16x32<F16>(rr16, res);
-                  else {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) res[i] = 0.f;
-                  }
-                } else if (valid) {
-                  load_f32x32(st.f_in + (size_t)r * st.ld_in + c0, res);
+                if (r16 || !valid) {
+                  cvt16x32<F16>(rr16, res);
                 } else {
-#pragma unroll
-                  for (int i = 0; i < 32; ++i) res[i] = 0.f;
+                  load_f32x32(rp32 + cc * 32, res);
                 }
                 lds_f32x32(sb + cc * 32, y);
                 tmem_wait32(ta);
@@ -938,20 +946,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
 #pragma unroll
                   for (int i = 0; i < 32; ++i) y[i] += gm[i];
                 }
-                if (valid) {
-                  if (st.flags & EF_STORE_F32) store_f32x32(st.f_out + (size_t)r * st.ld_out + c0, y);
-                  if (st.flags & EF_STORE_BF) st16x32<F16>(st.bf_out + (size_t)r * H + c0, y);
-                }
-                if (st.flags & EF_WRITE_ACT) store_tile32<H, false, F16>(act, C::ACT_HALF, trow, c0, y);
+                if (w32) store_f32x32(op32 + cc * 32, y);
+                if (w16) st16x32<F16>(op16 + cc * 32, y);
+                if (wact) store_tile32<H, false, F16>(act, C::ACT_HALF, trow, c0, y);
               }
-              wrote_act = (st.flags & EF_WRITE_ACT) != 0;
+              wrote_act = wact;
             } else if constexpr (BWD) {
-              // LayerNorm backward (see the SPLIT path for the formula)
-              const bool g16 = (st.flags & EF_G16) != 0;
+              // LayerNorm backward (formula as in the SPLIT path)
+              const bool g16 = (fl & EF_G16) != 0, csall = (fl & EF_COLSUM_ALL) != 0;
               const bool has_g = valid && r < st.valid_in;
-              const __nv_bfloat16* gp16 = st.g16 + (size_t)r * H + cb;
+              __nv_bfloat16* gp16 = st.g16 + (size_t)r * H + cb;
               const __nv_bfloat16* ap16 = st.ga16 + (size_t)dst * H + cb;
+              const float* gp32 = st.f_in + (size_t)r * st.ld_in + cb;
+              __nv_bfloat16* zp = st.scr_z + (size_t)r * H + cb;
               uint32_t g1[16], g2[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) { g1[i] = 0u; g2[i] = 0u; }
               float s1 = 0.f, s2 = 0.f;
               tmem_ld32_async(tl, ta);
               if (g16) {
@@ -963,18 +973,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
                 const int c0 = cb + cc * 32;
                 float dy[32], xh[32];
                 if (g16) {
-                  if (has_g) cvt16x32<F16>(g1, dy);
-                  else {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) dy[i] = 0.f;
-                  }
-                  if (valid) {
-                    add16x32<F16>(g2, dy);
-                    round16x32<F16>(dy);                      // as stored (G_e')
-                    st16x32<F16>(st.g16 + (size_t)r * H + c0, dy);
-                  }
+                  cvt16x32<F16>(g1, dy);
+                  add16x32<F16>(g2, dy);
+                  round16x32<F16>(dy);                      // as stored (G_e')
+                  if (valid) st16x32<F16>(gp16 + cc * 32, dy);
+                } else if (has_g) {
+                  load_f32x32(gp32 + cc * 32, dy);
                 } else {
-                  load_dy(st, has_g, valid, r, dst, c0, dy);
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) dy[i] = 0.f;
                 }
                 lds_f32x32(sb + cc * 32, xh);
                 tmem_wait32(ta);
@@ -989,22 +996,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
                 }
                 float gm[32];
                 lds_f32x32(sg + cc * 32, gm);
-                float t1[32], t2[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                   const float dxh = dy[i] * gm[i];
                   s1 += dxh;
                   s2 += dxh * xh[i];
-                  t1[i] = valid ? dy[i] * xh[i] : 0.f;
-                  t2[i] = valid ? dy[i] : 0.f;
+                  gm[i] = valid ? dy[i] * xh[i] : 0.f;               // reuse: dgamma terms
                 }
-                colsum_add(0, c0, t1);                               // dgamma
-                if (st.flags & EF_COLSUM_ALL) colsum_add(1, c0, t2);  // dbeta
+                colsum_add(0, c0, gm);                               // dgamma
+                if (csall) {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) xh[i] = valid ? dy[i] : 0.f;
+                  colsum_add(1, c0, xh);                             // dbeta
+                }
               }
               s1 = row_sum(s1) * (1.0f / H);
               s2 = row_sum(s2) * (1.0f / H);
               if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 4] = clock64();
               // pass B: dz = rstd (dxh - mean(dxh) - xh mean(dxh xh))
+#pragma unroll
+              for (int i = 0; i < 16; ++i) g1[i] = 0u;
               tmem_ld32_async(tl, ta);
               if (g16 && valid) ld16x32(gp16, g1);     // G_e' (written in pass A by this thread)
 #pragma unroll 1
@@ -1012,13 +1023,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
                 const int c0 = cb + cc * 32;
                 float dy[32], xh[32];
                 if (g16) {
-                  if (valid) cvt16x32<F16>(g1, dy);
-                  else {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) dy[i] = 0.f;
-                  }
+                  cvt16x32<F16>(g1, dy);
+                } else if (has_g) {
+                  load_f32x32(gp32 + cc * 32, dy);
                 } else {
-                  load_dy(st, has_g, valid, r, dst, c0, dy);
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) dy[i] = 0.f;
                 }
                 lds_f32x32(sb + cc * 32, xh);
                 tmem_wait32(ta);
@@ -1033,78 +1043,85 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) dy[i] = valid ? rstd * (dy[i] * gm[i] - s1 - xh[i] * s2) : 0.f;
                 store_tile32<H, false, F16>(act, C::ACT_HALF, trow, c0, dy);
-                if (valid) st16x32<F16>(st.scr_z + (size_t)r * H + c0, dy);
-                if (st.flags & EF_COLSUM_ALL) colsum_add(2, c0, dy);   // db_{m+1}
+                if (valid) st16x32<F16>(zp + cc * 32, dy);
+                if (csall) colsum_add(2, c0, dy);   // db_{m+1}
               }
               wrote_act = true;
             }
           } else if (op == EPI_DSILU) {
             if constexpr (BWD) {
+              const bool csall = (fl & EF_COLSUM_ALL) != 0;
+              const int vec = st.vec0;
               const __nv_bfloat16* sp = st.scr_s + (size_t)r * H + cb;
+              __nv_bfloat16* zp = st.scr_z + (size_t)r * H + cb;
               uint32_t sr[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) sr[i] = 0u;
               tmem_ld32_async(tl, ta);
               if (valid) ld16x32(sp, sr);
 #pragma unroll 1
               for (int cc = 0; cc < NC; ++cc) {
                 const int c0 = cb + cc * 32;
                 float x[32];
-                if (valid) cvt16x32<F16>(sr, x);
+                cvt16x32<F16>(sr, x);
                 tmem_wait32(ta);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) x[i] = valid ? x[i] * __uint_as_float(ta[i]) : 0.f;
+                for (int i = 0; i < 32; ++i) x[i] *= __uint_as_float(ta[i]);   // invalid rows: S' = 0
                 if (cc + 1 < NC) {
                   tmem_ld32_async(tl + (cc + 1) * 32, ta);
                   if (valid) ld16x32(sp + (cc + 1) * 32, sr);
                 }
                 store_tile32<H, false, F16>(act, C::ACT_HALF, trow, c0, x);
-                if (valid) st16x32<F16>(st.scr_z + (size_t)r * H + c0, x);
-                if (st.flags & EF_COLSUM_ALL) colsum_add(st.vec0, c0, x);
+                if (valid) st16x32<F16>(zp + cc * 32, x);
+                if (csall) colsum_add(vec, c0, x);
               }
               wrote_act = true;
             }
           } else if (op == EPI_STORE) {
+            const bool o16 = (fl & EF_OUT16) != 0;
+            __nv_bfloat16* op16 = st.bf_out + (size_t)r * st.ld_out + st.col0 + cb;
+            float* op32 = st.f_out + (size_t)r * st.ld_out + st.col0 + cb;
             tmem_ld32_async(tl, ta);
 #pragma unroll 1
             for (int cc = 0; cc < NC; ++cc) {
-              const int c0 = cb + cc * 32;
               tmem_wait32(ta);
               float x[32];
 #pragma unroll
               for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(ta[i]);
               if (cc + 1 < NC) tmem_ld32_async(tl + (cc + 1) * 32, ta);
               if (valid) {
-                if (st.flags & EF_OUT16) st16x32<F16>(st.bf_out + (size_t)r * st.ld_out + st.col0 + c0, x);
-                else store_f32x32(st.f_out + (size_t)r * st.ld_out + st.col0 + c0, x);
+                if (o16) st16x32<F16>(op16 + cc * 32, x);
+                else store_f32x32(op32 + cc * 32, x);
               }
             }
           } else if (op == EPI_ADD) {
-            const bool g16 = (st.flags & EF_G16) != 0;
+            const bool g16 = (fl & EF_G16) != 0, gg = (fl & EF_GATHER_G) != 0;
             const bool has_in = valid && r < st.valid_in;
             const __nv_bfloat16* ip = st.g16 + (size_t)r * H + cb;
+            __nv_bfloat16* op16 = st.g16_out + (size_t)r * H + cb;
+            const float* ip32 = st.f_in + (size_t)r * st.ld_in + cb;
+            const float* gp32 = st.gather + (size_t)dst * H + cb;
+            float* op32 = st.f_out + (size_t)r * st.ld_out + cb;
             uint32_t ir[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) ir[i] = 0u;
             tmem_ld32_async(tl, ta);
             if (g16 && valid) ld16x32(ip, ir);
 #pragma unroll 1
             for (int cc = 0; cc < NC; ++cc) {
-              const int c0 = cb + cc * 32;
               float x[32];
               if (g16) {
-                if (valid) cvt16x32<F16>(ir, x);
-                else {
-#pragma unroll
-                  for (int i = 0; i < 32; ++i) x[i] = 0.f;
-                }
-              } else if (has_in) {
-                load_f32x32(st.f_in + (size_t)r * st.ld_in + c0, x);
+                cvt16x32<F16>(ir, x);
               } else {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) x[i] = 0.f;
-              }
-              if (!g16 && valid && (st.flags & EF_GATHER_G)) {
-                float t[32];
-                load_f32x32(st.gather + (size_t)dst * H + c0, t);
+                if (has_in) load_f32x32(ip32 + cc * 32, x);
+                if (valid && gg) {
+                  float t[32];
+                  load_f32x32(gp32 + cc * 32, t);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) x[i] += t[i];
+                  for (int i = 0; i < 32; ++i) x[i] += t[i];
+                }
               }
               tmem_wait32(ta);
 #pragma unroll
@@ -1114,8 +1131,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
                 if (g16 && valid) ld16x32(ip + (cc + 1) * 32, ir);
               }
               if (valid) {
-                if (g16) st16x32<F16>(st.g16_out + (size_t)r * H + c0, x);
-                else store_f32x32(st.f_out + (size_t)r * st.ld_out + c0, x);
+                if (g16) st16x32<F16>(op16 + cc * 32, x);
+                else store_f32x32(op32 + cc * 32, x);
               }
             }
           }

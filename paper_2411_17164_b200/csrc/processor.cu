@@ -183,6 +183,7 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
   p.src = src;
   p.dst = dst;
   p.eps = ws->cfg.ln_eps;
+  { const char* d = getenv("XMGN_DBG"); p.dbg = d ? atoi(d) : 0; }
   const int n = pr.n;
   if (epi_writes_act(p.steps[n - 1])) throw Fail{set_error(XMGN_ESTATE, "internal: program ends writing ACT")};
   for (int s = 0; s < n; ++s) {
