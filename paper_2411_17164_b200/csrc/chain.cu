@@ -13,7 +13,7 @@ static void chain_launch(const ChainParams& p, int grid, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
     attr = true;
   }
-  kern<<<grid, CHAIN_THREADS, C::SMEM_BYTES, st>>>(p);
+  kern<<<grid, EpiShape<SPLIT>::THREADS, C::SMEM_BYTES, st>>>(p);
 }
 
 size_t chain_smem(int H, bool split) {

@@ -91,10 +91,29 @@ struct Step {
 constexpr int MAX_STEPS = 8;
 constexpr int MAX_MAPS = 8;
 constexpr int NV_MAX = 5;  // column-sum vectors per kernel
-// Epilogue: EPI_GROUPS warps per TMEM lane quadrant, each owning H/EPI_GROUPS
-// columns of its 32 rows (row statistics are exchanged through shared memory).
-constexpr int EPI_GROUPS = 2;
-constexpr int CHAIN_THREADS = 128 + 128 * EPI_GROUPS;
+// Epilogue: EW warps per TMEM lane quadrant, each owning H/EW columns of its 32
+// rows (row statistics are exchanged through shared memory).  The 16-bit modes
+// use four column groups (16 epilogue warps, latency tolerance); the FP32 check
+// mode keeps two (its hi/lo operands need the registers).
+#ifndef XMGN_EPI_GROUPS
+#define XMGN_EPI_GROUPS 4
+#endif
+#ifndef XMGN_EPI_SINGLE_ARRIVE
+#define XMGN_EPI_SINGLE_ARRIVE 1
+#endif
+template <bool SPLIT>
+struct EpiShape {
+  static constexpr int EW = SPLIT ? 2 : XMGN_EPI_GROUPS;
+  static constexpr int THREADS = 128 + 128 * EW;
+  // setmaxnreg split.  The CTA owns exactly THREADS x LAUNCH_REGS registers (the
+  // count ptxas derives from __launch_bounds__); setmaxnreg.inc can only take what
+  // the control warpgroup released with setmaxnreg.dec, or it blocks forever.
+  static constexpr int LAUNCH_REGS = (65536 / THREADS) & ~7;
+  static constexpr int CTRL_REGS = 56;
+  static constexpr int EPI_REGS_FIT = (LAUNCH_REGS + (LAUNCH_REGS - CTRL_REGS) / EW) & ~7;
+  static constexpr int EPI_REGS = EPI_REGS_FIT > 224 ? 224 : EPI_REGS_FIT;
+  static_assert(128 * CTRL_REGS + 128 * EW * EPI_REGS <= THREADS * LAUNCH_REGS, "register pool");
+};
 
 struct ChainParams {
   CUtensorMap maps[MAX_MAPS];
@@ -123,11 +142,11 @@ struct ChainCfg {
   static constexpr uint32_t B_SLOT = F * B_SLOT_HALF;
   static constexpr uint32_t SMEM_LIMIT = 227u * 1024u;
   static constexpr uint32_t PRM_BYTES = 2u * 3u * H * 4u;        // per-step bias/gamma/beta, double-buffered
-  static constexpr int SB_FIT = (int)((SMEM_LIMIT - 1536u - 512u * EPI_GROUPS - PRM_BYTES - ACT_BYTES) / B_SLOT);
+  static constexpr int SB_FIT = (int)((SMEM_LIMIT - 1536u - 512u * EpiShape<SPLIT>::EW - PRM_BYTES - ACT_BYTES) / B_SLOT);
   static constexpr int SB = SB_FIT > 8 ? 8 : SB_FIT;
   static constexpr uint32_t BAR_OFF = ACT_BYTES + SB * B_SLOT;
   static constexpr uint32_t RED_OFF = BAR_OFF + 512;             // row-reduction exchange [EW][128] f32
-  static constexpr uint32_t PRM_OFF = RED_OFF + EPI_GROUPS * 128 * 4;
+  static constexpr uint32_t PRM_OFF = RED_OFF + EpiShape<SPLIT>::EW * 128 * 4;
   static constexpr uint32_t SMEM_BYTES = PRM_OFF + PRM_BYTES + 1024;  // + alignment slack
   static constexpr uint32_t TMEM_COLS = H;
   static_assert(SB >= 2, "B ring too small");
@@ -267,46 +286,6 @@ __device__ __forceinline__ float warp_colsum32(float* v) {
   return v[0];
 }
 
-// ---- helpers of the pipelined 16-bit epilogue
-__device__ __forceinline__ void ld16x32(const __nv_bfloat16* p, uint32_t* r) {  // 32 x 16-bit (64 B)
-  ldg256(p, r);
-  ldg256(p + 16, r + 8);
-}
-template <bool F16>
-__device__ __forceinline__ void cvt16x32(const uint32_t* r, float* v) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) unpack8<F16>(make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]), v + 8 * q);
-}
-template <bool F16>
-__device__ __forceinline__ void add16x32(const uint32_t* r, float* v) {
-  float t[32];
-  cvt16x32<F16>(r, t);
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] += t[i];
-}
-template <bool F16>
-__device__ __forceinline__ void st16x32(__nv_bfloat16* p, const float* v) {
-  uint32_t h[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) h[i] = pack16<F16>(v[2 * i], v[2 * i + 1]);
-  stg256(p, h);
-  stg256(p + 16, h + 8);
-}
-template <bool F16>
-__device__ __forceinline__ void round16x32(float* v) {
-  uint32_t h[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) h[i] = pack16<F16>(v[2 * i], v[2 * i + 1]);
-  cvt16x32<F16>(h, v);
-}
-__device__ __forceinline__ void lds_f32x32(const float* p, float* v) {  // broadcast read
-  const uint32_t a = smem_u32(p);
-#pragma unroll
-  for (int q = 0; q < 8; ++q)
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v[4 * q]), "=f"(v[4 * q + 1]), "=f"(v[4 * q + 2]), "=f"(v[4 * q + 3])
-                 : "r"(a + 16 * q));
-}
 // SiLU(x) = h + h tanh(h), h = x/2.  FP16 mode: tanh on packed f16x2 (one MUFU op per
 // two elements; its ~2^-11 error is at the FP16 rounding of the stored activation).
 template <bool F16>
@@ -322,33 +301,6 @@ __device__ __forceinline__ void tanh2(float a, float b, float& ta, float& tb) {
     asm("tanh.approx.f32 %0, %1;" : "=f"(tb) : "f"(b));
   }
 }
-template <bool F16>
-__device__ __forceinline__ void silu32(float* x) {
-#pragma unroll
-  for (int i = 0; i < 32; i += 2) {
-    const float ha = 0.5f * x[i], hb = 0.5f * x[i + 1];
-    float ta, tb;
-    tanh2<F16>(ha, hb, ta, tb);
-    x[i] = fmaf(ha, ta, ha);
-    x[i + 1] = fmaf(hb, tb, hb);
-  }
-}
-// x <- SiLU(x), d <- SiLU'(x) = s + x s (1 - s), s = (1 + tanh(x/2)) / 2
-template <bool F16>
-__device__ __forceinline__ void silu_grad32(float* x, float* d) {
-#pragma unroll
-  for (int i = 0; i < 32; i += 2) {
-    const float ha = 0.5f * x[i], hb = 0.5f * x[i + 1];
-    float ta, tb;
-    tanh2<F16>(ha, hb, ta, tb);
-    const float sa = fmaf(0.5f, ta, 0.5f), sb2 = fmaf(0.5f, tb, 0.5f);
-    d[i] = fmaf(x[i] * sa, 1.0f - sa, sa);
-    d[i + 1] = fmaf(x[i + 1] * sb2, 1.0f - sb2, sb2);
-    x[i] = fmaf(ha, ta, ha);
-    x[i + 1] = fmaf(hb, tb, hb);
-  }
-}
-
 // dY of the LayerNorm backward: incoming gradient rows (< valid_in) plus the
 // aggregation adjoint G_a[dst] for edge programs.
 __device__ __forceinline__ void load_dy(const Step& st, bool has_g, bool valid, int r, int dst, int c0, float* dy) {
@@ -365,13 +317,18 @@ __device__ __forceinline__ void load_dy(const Step& st, bool has_g, bool valid, 
   }
 }
 
+}  // namespace xmgn
+#include "epi16.cuh"
+namespace xmgn {
+
 template <int H, bool SPLIT, bool BWD, bool F16>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THREADS, 1)
     k_chain(const __grid_constant__ ChainParams p) {
   using C = ChainCfg<H, SPLIT>;
   constexpr int NB = C::NB;
   constexpr int NH = H / NB;           // N-halves per step
-  constexpr int EW = EPI_GROUPS;
+  using ES = EpiShape<SPLIT>;
+  constexpr int EW = ES::EW;
   constexpr int HC = H / EW;           // columns per epilogue warp
   constexpr int NC = HC / 32;          // 32-column chunks per epilogue warp
   constexpr int NEPI = 128 * EW;       // epilogue threads
@@ -398,12 +355,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
   const int cid = (int)cluster_id_x(), ncl = (int)n_clusters_x();
   const int n_tiles = (p.M + 255) / 256;     // pair tiles of 256 rows (128 per CTA)
   constexpr int EPI_WARPS = NEPI / 32;
+  constexpr int EPI_ARRIVALS = XMGN_EPI_SINGLE_ARRIVE ? 1 : EPI_WARPS;
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::SA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < C::SB; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
     mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 2 * EPI_WARPS);   // one arrival per epilogue warp of both CTAs
-    mbar_init(act_full, 2 * EPI_WARPS);
+    mbar_init(acc_empty, 2 * EPI_ARRIVALS);   // epilogue arrivals of both CTAs
+    mbar_init(act_full, 2 * EPI_ARRIVALS);
     mbar_init(act_free, 1);
     mbar_init(mma_idle, 1);
     fence_barrier_init();
@@ -416,11 +374,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  if (p.dbg > 0) {
+    // experiment: stagger the start of clusters by (cid % 4) * dbg microseconds so the
+    // pairs' memory-heavy epilogue phases do not all coincide
+    const unsigned long long t0 = clock64();
+    const unsigned long long wait_cyc = (unsigned long long)(cid % 4) * (unsigned long long)p.dbg * 1900ull;
+    while (clock64() - t0 < wait_cyc) __nanosleep(1000);
+  }
 
   // register split (setmaxnreg, per warpgroup): control warps 0-3 need few registers,
   // the epilogue warpgroups get the rest
   if (w < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(ES::CTRL_REGS) : "memory");
   if (w == 0) {
     // ============================ TMA producer (both CTAs: own A rows, own half of B)
     if (elect_one()) {
@@ -535,7 +500,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
     }
   }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(ES::EPI_REGS) : "memory");
     // ============================ epilogue: thread = tile row (TMEM lane) x HC columns
     const int q = w & 3;                 // TMEM lane quadrant
     const int eg = (w - 4) >> 2;         // column group
@@ -578,20 +543,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
       for (int s = 0; s < p.n_steps; ++s, ++g) {
         const Step& st = p.steps[s];
         float* prm = prm_base + (g & 1) * 3 * H;
-        if constexpr (!SPLIT) {
-          // stage this step's bias / gamma / beta into shared memory while the MMAs run
-          const int et = threadIdx.x - 128;
-          for (int i = et; i < 3 * H; i += NEPI) {
-            const float* srcv = i < H ? st.bias : (i < 2 * H ? st.gamma : st.beta);
-            prm[i] = srcv ? __ldg(srcv + (i % H)) : 0.f;
-          }
-          named_bar(7, NEPI);
-        }
+        bool wrote_act = false;
+        if constexpr (SPLIT) {
         mbar_wait(acc_full, g & 1);
         tc_fence_after();
         if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 2] = clock64();
-        bool wrote_act = false;
-        if constexpr (SPLIT) {
         float v[32], pb[32];
         if (st.epi == EPI_SILU && !(st.flags & (EF_GATHER_P | EF_STORE_S | EF_STORE_A))) {
           // plain SiLU epilogue, software-pipelined one chunk ahead (TMEM + bias)
@@ -842,298 +798,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
           }
         }
         } else {
-          // ---------------- software-pipelined epilogue (16-bit operand modes)
-          // Each op: the step's fields are read once into registers, parameter vectors come
-          // from shared memory, and TMEM + 16-bit row inputs are prefetched one 32-column
-          // chunk ahead.  Arrays are defined unconditionally (invalid rows load zeros).
-          const float* sb = prm + cb;            // bias
-          const float* sg = prm + H + cb;        // gamma
-          const float* sbt = prm + 2 * H + cb;   // beta
+          // ---------------- 16-bit operand modes: ops of epi16.cuh.  Each op issues its
+          // MMA-independent row loads, then calls wait(): stage this step's bias / gamma /
+          // beta in shared memory, wait for the accumulator.
+          auto wait = [&]() {
+            const int et = threadIdx.x - 128;
+            for (int i = et; i < 3 * H; i += NEPI) {
+              const float* srcv = i < H ? st.bias : (i < 2 * H ? st.gamma : st.beta);
+              prm[i] = srcv ? __ldg(srcv + (i % H)) : 0.f;
+            }
+            named_bar(7, NEPI);
+            mbar_wait(acc_full, g & 1);
+            tc_fence_after();
+            if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 2] = clock64();
+          };
+          Epi e;
+          e.act = act; e.tl = tl; e.trow = trow; e.cb = cb; e.r = r; e.src = src; e.dst = dst; e.valid = valid;
+          e.sb = prm + cb; e.sg = prm + H + cb; e.sbt = prm + 2 * H + cb; e.colsum = colsum_base; e.eps = p.eps;
+          constexpr int NC16 = HC / 16;
           const int op = st.epi;
-          const int fl = st.flags;
-          uint32_t ta[32];
           if (op == EPI_SILU) {
-            const bool gp = (fl & EF_GATHER_P) != 0;
-            const bool sa = valid && (fl & EF_STORE_A) != 0, ss = (fl & EF_STORE_S) != 0;
-            const __nv_bfloat16* ps = st.gather16 + (size_t)src * 2 * H + cb;
-            const __nv_bfloat16* pd = st.gather16 + (size_t)dst * 2 * H + H + cb;
-            __nv_bfloat16* oa = st.scr_a + (size_t)r * H + cb;
-            __nv_bfloat16* os = st.scr_s + (size_t)r * H + cb;
-            uint32_t gs[16], gd[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) { gs[i] = 0u; gd[i] = 0u; }
-            tmem_ld32_async(tl, ta);
-            if (gp) { ld16x32(ps, gs); ld16x32(pd, gd); }
-#pragma unroll 1
-            for (int cc = 0; cc < NC; ++cc) {
-              const int c0 = cb + cc * 32;
-              float x[32];
-              lds_f32x32(sb + cc * 32, x);
-              add16x32<F16>(gs, x);
-              add16x32<F16>(gd, x);
-              tmem_wait32(ta);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) x[i] += __uint_as_float(ta[i]);
-              if (cc + 1 < NC) {
-                tmem_ld32_async(tl + (cc + 1) * 32, ta);
-                if (gp) { ld16x32(ps + (cc + 1) * 32, gs); ld16x32(pd + (cc + 1) * 32, gd); }
-              }
-              if (ss) {
-                float dv[32];
-                silu_grad32<F16>(x, dv);          // x <- SiLU(x), dv <- SiLU'(x)
-                if (valid) st16x32<F16>(os + cc * 32, dv);
-              } else {
-                silu32<F16>(x);
-              }
-              store_tile32<H, false, F16>(act, C::ACT_HALF, trow, c0, x);
-              if (sa) st16x32<F16>(oa + cc * 32, x);
-            }
+            op_silu<H, NC16, F16>(e, st, wait);
             wrote_act = true;
-          } else if (op == EPI_LN_FWD || op == EPI_LN_BWD) {
-            // one TMEM pass for mean / E[z^2]
-            float sum = 0.f, sq = 0.f;
-            tmem_ld32_async(tl, ta);
-#pragma unroll 1
-            for (int cc = 0; cc < NC; ++cc) {
-              float b[32];
-              lds_f32x32(sb + cc * 32, b);
-              tmem_wait32(ta);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) b[i] += __uint_as_float(ta[i]);
-              if (cc + 1 < NC) tmem_ld32_async(tl + (cc + 1) * 32, ta);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) { sum += b[i]; sq = fmaf(b[i], b[i], sq); }
-            }
-            const float mean = row_sum(sum) * (1.0f / H);
-            const float var = fmaxf(row_sum(sq) * (1.0f / H) - mean * mean, 0.f);
-            const float rstd = rsqrtf(var + p.eps);
-            if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 3] = clock64();
-            if (op == EPI_LN_FWD) {
-              const bool r16 = (fl & EF_RES16) != 0, w32 = valid && (fl & EF_STORE_F32) != 0;
-              const bool w16 = valid && (fl & EF_STORE_BF) != 0, wact = (fl & EF_WRITE_ACT) != 0;
-              const __nv_bfloat16* rp = st.res16 + (size_t)r * H + cb;
-              const float* rp32 = st.f_in + (size_t)r * st.ld_in + cb;
-              float* op32 = st.f_out + (size_t)r * st.ld_out + cb;
-              __nv_bfloat16* op16 = st.bf_out + (size_t)r * H + cb;
-              uint32_t rr16[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) rr16[i] = 0u;
-              tmem_ld32_async(tl, ta);
-              if (r16 && valid) ld16x32(rp, rr16);
-#pragma unroll 1
-              for (int cc = 0; cc < NC; ++cc) {
-                const int c0 = cb + cc * 32;
-                float y[32], res[32];
-                if (r16 || !valid) {
-                  cvt16x32<F16>(rr16, res);
-                } else {
-                  load_f32x32(rp32 + cc * 32, res);
-                }
-                lds_f32x32(sb + cc * 32, y);
-                tmem_wait32(ta);
-#pragma unroll
-                for (int i = 0; i < 32; ++i) y[i] = (y[i] + __uint_as_float(ta[i]) - mean) * rstd;
-                if (cc + 1 < NC) {
-                  tmem_ld32_async(tl + (cc + 1) * 32, ta);
-                  if (r16 && valid) ld16x32(rp + (cc + 1) * 32, rr16);
-                }
-                {
-                  float gm[32];
-                  lds_f32x32(sg + cc * 32, gm);
-#pragma unroll
-                  for (int i = 0; i < 32; ++i) y[i] = fmaf(gm[i], y[i], res[i]);
-                  lds_f32x32(sbt + cc * 32, gm);
-#pragma unroll
-                  for (int i = 0; i < 32; ++i) y[i] += gm[i];
-                }
-                if (w32) store_f32x32(op32 + cc * 32, y);
-                if (w16) st16x32<F16>(op16 + cc * 32, y);
-                if (wact) store_tile32<H, false, F16>(act, C::ACT_HALF, trow, c0, y);
-              }
-              wrote_act = wact;
-            } else if constexpr (BWD) {
-              // LayerNorm backward (formula as in the SPLIT path)
-              const bool g16 = (fl & EF_G16) != 0, csall = (fl & EF_COLSUM_ALL) != 0;
-              const bool has_g = valid && r < st.valid_in;
-              __nv_bfloat16* gp16 = st.g16 + (size_t)r * H + cb;
-              const __nv_bfloat16* ap16 = st.ga16 + (size_t)dst * H + cb;
-              const float* gp32 = st.f_in + (size_t)r * st.ld_in + cb;
-              __nv_bfloat16* zp = st.scr_z + (size_t)r * H + cb;
-              uint32_t g1[16], g2[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) { g1[i] = 0u; g2[i] = 0u; }
-              float s1 = 0.f, s2 = 0.f;
-              tmem_ld32_async(tl, ta);
-              if (g16) {
-                if (has_g) ld16x32(gp16, g1);
-                if (valid) ld16x32(ap16, g2);
-              }
-#pragma unroll 1
-              for (int cc = 0; cc < NC; ++cc) {
-                const int c0 = cb + cc * 32;
-                float dy[32], xh[32];
-                if (g16) {
-                  cvt16x32<F16>(g1, dy);
-                  add16x32<F16>(g2, dy);
-                  round16x32<F16>(dy);                      // as stored (G_e')
-                  if (valid) st16x32<F16>(gp16 + cc * 32, dy);
-                } else if (has_g) {
-                  load_f32x32(gp32 + cc * 32, dy);
-                } else {
-#pragma unroll
-                  for (int i = 0; i < 32; ++i) dy[i] = 0.f;
-                }
-                lds_f32x32(sb + cc * 32, xh);
-                tmem_wait32(ta);
-#pragma unroll
-                for (int i = 0; i < 32; ++i) xh[i] = (xh[i] + __uint_as_float(ta[i]) - mean) * rstd;
-                if (cc + 1 < NC) {
-                  tmem_ld32_async(tl + (cc + 1) * 32, ta);
-                  if (g16) {
-                    if (has_g) ld16x32(gp16 + (cc + 1) * 32, g1);
-                    if (valid) ld16x32(ap16 + (cc + 1) * 32, g2);
-                  }
-                }
-                float gm[32];
-                lds_f32x32(sg + cc * 32, gm);
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  const float dxh = dy[i] * gm[i];
-                  s1 += dxh;
-                  s2 += dxh * xh[i];
-                  gm[i] = valid ? dy[i] * xh[i] : 0.f;               // reuse: dgamma terms
-                }
-                colsum_add(0, c0, gm);                               // dgamma
-                if (csall) {
-#pragma unroll
-                  for (int i = 0; i < 32; ++i) xh[i] = valid ? dy[i] : 0.f;
-                  colsum_add(1, c0, xh);                             // dbeta
-                }
-              }
-              s1 = row_sum(s1) * (1.0f / H);
-              s2 = row_sum(s2) * (1.0f / H);
-              if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 4] = clock64();
-              // pass B: dz = rstd (dxh - mean(dxh) - xh mean(dxh xh))
-#pragma unroll
-              for (int i = 0; i < 16; ++i) g1[i] = 0u;
-              tmem_ld32_async(tl, ta);
-              if (g16 && valid) ld16x32(gp16, g1);     // G_e' (written in pass A by this thread)
-#pragma unroll 1
-              for (int cc = 0; cc < NC; ++cc) {
-                const int c0 = cb + cc * 32;
-                float dy[32], xh[32];
-                if (g16) {
-                  cvt16x32<F16>(g1, dy);
-                } else if (has_g) {
-                  load_f32x32(gp32 + cc * 32, dy);
-                } else {
-#pragma unroll
-                  for (int i = 0; i < 32; ++i) dy[i] = 0.f;
-                }
-                lds_f32x32(sb + cc * 32, xh);
-                tmem_wait32(ta);
-#pragma unroll
-                for (int i = 0; i < 32; ++i) xh[i] = (xh[i] + __uint_as_float(ta[i]) - mean) * rstd;
-                if (cc + 1 < NC) {
-                  tmem_ld32_async(tl + (cc + 1) * 32, ta);
-                  if (g16 && valid) ld16x32(gp16 + (cc + 1) * 32, g1);
-                }
-                float gm[32];
-                lds_f32x32(sg + cc * 32, gm);
-#pragma unroll
-                for (int i = 0; i < 32; ++i) dy[i] = valid ? rstd * (dy[i] * gm[i] - s1 - xh[i] * s2) : 0.f;
-                store_tile32<H, false, F16>(act, C::ACT_HALF, trow, c0, dy);
-                if (valid) st16x32<F16>(zp + cc * 32, dy);
-                if (csall) colsum_add(2, c0, dy);   // db_{m+1}
-              }
-              wrote_act = true;
-            }
-          } else if (op == EPI_DSILU) {
-            if constexpr (BWD) {
-              const bool csall = (fl & EF_COLSUM_ALL) != 0;
-              const int vec = st.vec0;
-              const __nv_bfloat16* sp = st.scr_s + (size_t)r * H + cb;
-              __nv_bfloat16* zp = st.scr_z + (size_t)r * H + cb;
-              uint32_t sr[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) sr[i] = 0u;
-              tmem_ld32_async(tl, ta);
-              if (valid) ld16x32(sp, sr);
-#pragma unroll 1
-              for (int cc = 0; cc < NC; ++cc) {
-                const int c0 = cb + cc * 32;
-                float x[32];
-                cvt16x32<F16>(sr, x);
-                tmem_wait32(ta);
-#pragma unroll
-                for (int i = 0; i < 32; ++i) x[i] *= __uint_as_float(ta[i]);   // invalid rows: S' = 0
-                if (cc + 1 < NC) {
-                  tmem_ld32_async(tl + (cc + 1) * 32, ta);
-                  if (valid) ld16x32(sp + (cc + 1) * 32, sr);
-                }
-                store_tile32<H, false, F16>(act, C::ACT_HALF, trow, c0, x);
-                if (valid) st16x32<F16>(zp + cc * 32, x);
-                if (csall) colsum_add(vec, c0, x);
-              }
-              wrote_act = true;
-            }
+          } else if (op == EPI_LN_FWD) {
+            if (st.flags & EF_RES16) op_ln_fwd<H, NC16, F16, false>(e, st, wait, row_sum);
+            else op_ln_fwd<H, NC16, F16, true>(e, st, wait, row_sum);
+            wrote_act = (st.flags & EF_WRITE_ACT) != 0;
           } else if (op == EPI_STORE) {
-            const bool o16 = (fl & EF_OUT16) != 0;
-            __nv_bfloat16* op16 = st.bf_out + (size_t)r * st.ld_out + st.col0 + cb;
-            float* op32 = st.f_out + (size_t)r * st.ld_out + st.col0 + cb;
-            tmem_ld32_async(tl, ta);
-#pragma unroll 1
-            for (int cc = 0; cc < NC; ++cc) {
-              tmem_wait32(ta);
-              float x[32];
-#pragma unroll
-              for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(ta[i]);
-              if (cc + 1 < NC) tmem_ld32_async(tl + (cc + 1) * 32, ta);
-              if (valid) {
-                if (o16) st16x32<F16>(op16 + cc * 32, x);
-                else store_f32x32(op32 + cc * 32, x);
-              }
-            }
+            op_store<H, NC16, F16>(e, st, wait);
           } else if (op == EPI_ADD) {
-            const bool g16 = (fl & EF_G16) != 0, gg = (fl & EF_GATHER_G) != 0;
-            const bool has_in = valid && r < st.valid_in;
-            const __nv_bfloat16* ip = st.g16 + (size_t)r * H + cb;
-            __nv_bfloat16* op16 = st.g16_out + (size_t)r * H + cb;
-            const float* ip32 = st.f_in + (size_t)r * st.ld_in + cb;
-            const float* gp32 = st.gather + (size_t)dst * H + cb;
-            float* op32 = st.f_out + (size_t)r * st.ld_out + cb;
-            uint32_t ir[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) ir[i] = 0u;
-            tmem_ld32_async(tl, ta);
-            if (g16 && valid) ld16x32(ip, ir);
-#pragma unroll 1
-            for (int cc = 0; cc < NC; ++cc) {
-              float x[32];
-              if (g16) {
-                cvt16x32<F16>(ir, x);
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) x[i] = 0.f;
-                if (has_in) load_f32x32(ip32 + cc * 32, x);
-                if (valid && gg) {
-                  float t[32];
-                  load_f32x32(gp32 + cc * 32, t);
-#pragma unroll
-                  for (int i = 0; i < 32; ++i) x[i] += t[i];
-                }
-              }
-              tmem_wait32(ta);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) x[i] += __uint_as_float(ta[i]);
-              if (cc + 1 < NC) {
-                tmem_ld32_async(tl + (cc + 1) * 32, ta);
-                if (g16 && valid) ld16x32(ip + (cc + 1) * 32, ir);
-              }
-              if (valid) {
-                if (g16) st16x32<F16>(op16 + cc * 32, x);
-                else store_f32x32(op32 + cc * 32, x);
-              }
+            if (st.flags & EF_G16) op_add16<H, NC16, F16>(e, st, wait);
+            else op_add32<H, NC16, F16>(e, st, wait);
+          } else if constexpr (BWD) {
+            if (op == EPI_LN_BWD) {
+              if (st.flags & EF_G16) op_ln_bwd16<H, NC16, F16>(e, st, wait, row_sum);
+              else op_ln_bwd32<H, NC16, F16>(e, st, wait, row_sum);
+              wrote_act = true;
+            } else if (op == EPI_DSILU) {
+              op_dsilu<H, NC16, F16>(e, st, wait);
+              wrote_act = true;
             }
           }
         }
@@ -1141,10 +844,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CHAIN_THREADS, 1)
         if (wrote_act) fence_proxy_async_smem();
         __syncwarp();
         if (p.trace && blockIdx.x == 0 && g < 64 && lane == 0 && (w == 4 || w == 8)) p.trace[g * 8 + (w == 4 ? 5 : 6)] = clock64();
+#if XMGN_EPI_SINGLE_ARRIVE
+        // one release-arrive per CTA after the epilogue warps synchronise: only this
+        // warp's global stores sit in front of its release fence
+        named_bar(8, NEPI);
+        if (threadIdx.x == 128) {
+          mbar_arrive_cluster(acc_empty_l);
+          if (wrote_act) mbar_arrive_cluster(act_full_l);
+        }
+#else
         if (lane == 0) {
           mbar_arrive_cluster(acc_empty_l);
           if (wrote_act) mbar_arrive_cluster(act_full_l);
         }
+#endif
       }
     }
   }

@@ -14,6 +14,13 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+// mbarrier.try_wait suspend-time hint (ns): a waiting thread sleeps until the phase
+// completes (or the hint expires) instead of re-issuing try_wait, leaving issue slots
+// to the epilogue warps that share its scheduler.
+#ifndef XMGN_WAIT_HINT
+#define XMGN_WAIT_HINT 0x989680
+#endif
+
 namespace xmgn {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -49,9 +56,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n"
       "WAIT_%=:\n\t"
+#if XMGN_WAIT_HINT
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%0], %1, %2;\n\t"
+#else
       "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%0], %1;\n\t"
+#endif
       "@!P bra WAIT_%=;\n\t}\n" ::"r"(a),
-      "r"(parity)
+      "r"(parity), "r"(XMGN_WAIT_HINT)
       : "memory");
 }
 
@@ -301,6 +312,18 @@ __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t&
   } else {
     hi = pack16<F16>(a, b);
     lo = 0;
+  }
+}
+template <bool F16>
+__device__ __forceinline__ void unpack2(uint32_t u, float* v) {
+  if constexpr (F16) {
+    const __half2 h = *reinterpret_cast<const __half2*>(&u);
+    v[0] = __low2float(h);
+    v[1] = __high2float(h);
+  } else {
+    const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&u);
+    v[0] = __low2float(h);
+    v[1] = __high2float(h);
   }
 }
 template <bool F16>
