@@ -86,10 +86,14 @@ struct Step {
   __nv_bfloat16* g16_out;         // EPI_ADD + EF_G16 output (same lo offset as g16)
   const __nv_bfloat16* ga16;      // 16-bit aggregation adjoint G_a [N][H] gathered by dst (EF_G16)
   long long ga16_lo;
+  // 16-bit modes: the epilogue's contiguous 16-bit row input (S', G_e, G_e', residual) is
+  // bulk-loaded by TMA into the ACT tile once the accumulator is ready (ACT is dead then:
+  // the step's MMAs have read it); map slot, -1 = read rows from global instead
+  int in_map;
 };
 
 constexpr int MAX_STEPS = 8;
-constexpr int MAX_MAPS = 8;
+constexpr int MAX_MAPS = 16;
 constexpr int NV_MAX = 5;  // column-sum vectors per kernel
 // Epilogue: EW warps per TMEM lane quadrant, each owning H/EW columns of its 32
 // rows (row statistics are exchanged through shared memory).  The 16-bit modes
@@ -346,7 +350,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
   uint64_t* act_full = acc_empty + 1;        // epilogue -> MMA (ACT written)
   uint64_t* act_free = act_full + 1;         // MMA -> producer (no MMA reads ACT any more)
   uint64_t* mma_idle = act_free + 1;         // MMA -> itself (all issued MMAs retired)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(mma_idle + 1);
+  uint64_t* in_full = mma_idle + 1;          // [H/64] epilogue input boxes landed in ACT
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(in_full + H / 64);
   float* red = reinterpret_cast<float*>(smem + C::RED_OFF);
   float* prm_base = reinterpret_cast<float*>(smem + C::PRM_OFF);
 
@@ -364,6 +369,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
     mbar_init(act_full, 2 * EPI_ARRIVALS);
     mbar_init(act_free, 1);
     mbar_init(mma_idle, 1);
+    for (int i = 0; i < H / 64; ++i) mbar_init(&in_full[i], 1);
     fence_barrier_init();
   }
   if (w == 0 && lane_id() == 0)
@@ -436,6 +442,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         for (int s = 0; s < p.n_steps; ++s, ++g) {
           const Step& st = p.steps[s];
           const bool tma_a = st.a_src == A_TMA;
+          // the previous epilogue must be done (it may still read its input out of ACT)
+          // before ACT can become A-ring space again
+          if (g > 0) mbar_wait(acc_empty, (g - 1) & 1);
           if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) {
             // let every issued MMA (the ones reading ACT) retire, then hand both
             // CTAs' ACT tiles to their producers as A-ring space.
@@ -446,7 +455,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
             if (elect_one()) { mbar_arrive(act_free); mbar_arrive_cluster(act_free_peer); }
             __syncwarp();
           }
-          if (g > 0) mbar_wait(acc_empty, (g - 1) & 1);
           if (st.ctl & CTL_WAIT_ACT) { mbar_wait(act_full, nact & 1); ++nact; }
           tc_fence_after();
           if (p.trace && blockIdx.x == 0 && g < 64 && lane_id() == 0) p.trace[g * 8 + 0] = clock64();
@@ -533,7 +541,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
     };
     const uint32_t acc_empty_l = mapa_shared(smem_u32(acc_empty), 0);
     const uint32_t act_full_l = mapa_shared(smem_u32(act_full), 0);
-    int g = 0;
+    int g = 0, nin = 0;   // nin: steps whose input came through in_full (its phase)
     for (int tile = cid; tile < n_tiles; tile += ncl) {
       const int r = tile * 256 + (int)rank * 128 + trow;
       const bool valid = r < p.M;
@@ -811,10 +819,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
             mbar_wait(acc_full, g & 1);
             tc_fence_after();
             if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 2] = clock64();
+            if (st.in_map >= 0 && threadIdx.x == 128) {
+              // the step's MMAs have read ACT: bulk-load the row input over it, in the order
+              // the column groups consume the 64-column boxes
+              const int row0 = tile * 256 + (int)rank * 128;
+              constexpr int BPG = HC >= 64 ? HC / 64 : 1;          // boxes per column group
+              constexpr int NG = HC >= 64 ? EW : H / 64;
+              for (int j = 0; j < BPG; ++j)
+                for (int gi = 0; gi < NG; ++gi) {
+                  const int b = gi * BPG + j;
+                  mbar_expect_tx(&in_full[b], 128 * 128);
+                  tma_load_2d(act + b * (128 * 128), &p.maps[st.in_map], &in_full[b], b * 64, row0);
+                }
+            }
           };
           Epi e;
           e.act = act; e.tl = tl; e.trow = trow; e.cb = cb; e.r = r; e.src = src; e.dst = dst; e.valid = valid;
           e.sb = prm + cb; e.sg = prm + H + cb; e.sbt = prm + 2 * H + cb; e.colsum = colsum_base; e.eps = p.eps;
+          e.in_full = in_full; e.in_par = nin & 1;
           constexpr int NC16 = HC / 16;
           const int op = st.epi;
           if (op == EPI_SILU) {
@@ -839,6 +861,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
               wrote_act = true;
             }
           }
+          if (st.in_map >= 0) ++nin;
         }
         tc_fence_before();
         if (wrote_act) fence_proxy_async_smem();

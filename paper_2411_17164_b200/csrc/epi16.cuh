@@ -165,7 +165,16 @@ struct Epi {
   const float* sbt;  // beta  [cb ..]
   float* colsum;     // per-(CTA, quadrant) column-sum partials [NV_MAX][H] (backward)
   float eps;
+  uint64_t* in_full; // [H/64] mbarriers: TMA-loaded input boxes in ACT (Step::in_map)
+  uint32_t in_par;   // their phase parity for this step
 };
+
+// 16 values of this row's TMA-loaded input (ACT, columns c0 .. c0+15), after the box landed
+template <bool F16>
+__device__ __forceinline__ void in16(const Epi& e, int c0, float* v) {
+  mbar_wait(&e.in_full[c0 >> 6], e.in_par);
+  lds_tile16<F16>(e.act, e.trow, c0, v);
+}
 
 template <int H>
 __device__ __forceinline__ void colsum16_add(const Epi& e, int vec, int c0, float* vals) {
@@ -281,7 +290,8 @@ __device__ __forceinline__ void op_ln_fwd(const Epi& e, const Step& st, Wait wai
     if constexpr (IN32) ld32x16(rp32 + cc * 16, q);
     else ld16(rp16 + cc * 16, q);
   };
-  if (has_res) { load(0, q0); if (!IN32) load(1, q1); }
+  const bool tin = !IN32 && st.in_map >= 0;    // residual rows arrive in ACT by TMA
+  if (has_res && !tin) { load(0, q0); if (!IN32) load(1, q1); }
   wait();
   float mean, rstd;
   ln_stats16<H, NC>(e, e.eps, row_sum, mean, rstd);
@@ -293,9 +303,10 @@ __device__ __forceinline__ void op_ln_fwd(const Epi& e, const Step& st, Wait wai
 #pragma unroll
       for (int i = 0; i < 16; ++i) res[i] = __uint_as_float(q[i]);
     } else {
-      cvt16<F16>(q, res);
+      if (tin) in16<F16>(e, e.cb + cc * 16, res);   // rows >= M read zero (OOB fill)
+      else cvt16<F16>(q, res);
     }
-    if (has_res && cc + AHEAD < NC) load(cc + AHEAD, q);
+    if (has_res && !tin && cc + AHEAD < NC) load(cc + AHEAD, q);
     lds16(e.sb + cc * 16, y);
     tmem_wait16(ta);
 #pragma unroll
@@ -333,7 +344,8 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
   uint32_t g0[8], g1[8], a0[8], a1[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) g0[i] = g1[i] = a0[i] = a1[i] = 0u;
-  if (has_g) { ld16(gp16, g0); ld16(gp16 + 16, g1); }
+  const bool tin = st.in_map >= 0;   // G_e rows arrive in ACT by TMA (rows >= valid_in read zero)
+  if (has_g && !tin) { ld16(gp16, g0); ld16(gp16 + 16, g1); }
   if (e.valid) { ld16(ap16, a0); ld16(ap16 + 16, a1); }
   wait();
   float mean, rstd;
@@ -344,10 +356,11 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
   auto passA = [&](int cc, uint32_t* gq, uint32_t* aq) {
     const int c0 = e.cb + cc * 16;
     float dy[16], xh[16];
-    cvt16<F16>(gq, dy);
+    if (tin) in16<F16>(e, c0, dy);
+    else cvt16<F16>(gq, dy);
     add16<F16>(aq, dy);
     if (cc + 2 < NC) {
-      if (has_g) ld16(gp16 + (cc + 2) * 16, gq);
+      if (has_g && !tin) ld16(gp16 + (cc + 2) * 16, gq);
       if (e.valid) ld16(ap16 + (cc + 2) * 16, aq);
     }
     round16<F16>(dy);                                // as stored (G_e')
@@ -490,15 +503,17 @@ __device__ __forceinline__ void op_dsilu(const Epi& e, const Step& st, Wait wait
   uint32_t q0[8], q1[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) q0[i] = q1[i] = 0u;   // invalid rows: S' = 0
-  if (e.valid) { ld16(sp, q0); ld16(sp + 16, q1); }
+  const bool tin = st.in_map >= 0;   // S' rows arrive in ACT by TMA
+  if (e.valid && !tin) { ld16(sp, q0); ld16(sp + 16, q1); }
   wait();
   uint32_t ta[16];
   tmem_ld16_async(e.tl, ta);
   auto body = [&](int cc, uint32_t* q) {
     const int c0 = e.cb + cc * 16;
     float x[16];
-    cvt16<F16>(q, x);
-    if (e.valid && cc + 2 < NC) ld16(sp + (cc + 2) * 16, q);
+    if (tin) in16<F16>(e, c0, x);       // rows >= M read zero
+    else cvt16<F16>(q, x);
+    if (e.valid && !tin && cc + 2 < NC) ld16(sp + (cc + 2) * 16, q);
     tmem_wait16(ta);
 #pragma unroll
     for (int i = 0; i < 16; ++i) x[i] *= __uint_as_float(ta[i]);
@@ -545,14 +560,16 @@ __device__ __forceinline__ void op_add16(const Epi& e, const Step& st, Wait wait
   uint32_t q0[8], q1[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) q0[i] = q1[i] = 0u;
-  if (e.valid) { ld16(ip, q0); ld16(ip + 16, q1); }
+  const bool tin = st.in_map >= 0;   // G_e' rows arrive in ACT by TMA
+  if (e.valid && !tin) { ld16(ip, q0); ld16(ip + 16, q1); }
   wait();
   uint32_t ta[16];
   tmem_ld16_async(e.tl, ta);
   auto body = [&](int cc, uint32_t* q) {
     float x[16];
-    cvt16<F16>(q, x);
-    if (e.valid && cc + 2 < NC) ld16(ip + (cc + 2) * 16, q);
+    if (tin) in16<F16>(e, e.cb + cc * 16, x);
+    else cvt16<F16>(q, x);
+    if (e.valid && !tin && cc + 2 < NC) ld16(ip + (cc + 2) * 16, q);
     tmem_wait16(ta);
 #pragma unroll
     for (int i = 0; i < 16; ++i) x[i] += __uint_as_float(ta[i]);

@@ -156,12 +156,21 @@ static CUtensorMap map_rows(const bf16* base, long long rows, int width, int box
 struct Prog {
   ChainParams p;
   int n = 0;
+  int next_map = 8;   // map slots 8.. hold the epilogues' TMA row inputs
   Prog() { std::memset(&p, 0, sizeof(p)); }
   Step& add() {
     Step& s = p.steps[n++];
     std::memset(&s, 0, sizeof(s));
     s.a_map1 = -1;
+    s.in_map = -1;
     return s;
+  }
+  // TMA source of an epilogue row input: 16-bit rows [0, rows) x H, rows > 0 (rows beyond read zero)
+  int in_map(const bf16* base, long long rows, int H) {
+    if (next_map >= MAX_MAPS) throw Fail{set_error(XMGN_ESTATE, "internal: out of tensor-map slots")};
+    if (rows <= 0) throw Fail{set_error(XMGN_ESTATE, "internal: empty TMA input map")};
+    p.maps[next_map] = tmap_bf16(base, H, (uint64_t)rows, H, 64, 128);
+    return next_map++;
   }
 };
 
@@ -484,6 +493,7 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
         s.gamma = params + Ly.gamma(li, 0); s.beta = params + Ly.beta(li, 0);
         s.flags = EF_RES16 | EF_STORE_BF;
         s.res16 = eck_prev.p; s.res16_lo = eck_prev.lo;
+        if (!ws->split) s.in_map = pr.in_map(eck_prev.p, el, H);   // residual e^{l-1} rows
         s.bf_out = eck_next.p; s.bf_lo = eck_next.lo;
         run_prog(ws, "chain_edge_fwd", pr, (int)el, dp.src, dp.dst, false, st);
       }
@@ -559,6 +569,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
       BfBuf ack = at(ws->a_ck, (long long)li * NH);
       // common recompute + dgrad program of an MLP block (blk 0 edge, 1 node)
       auto mlp_bwd = [&](Prog& pr, int blk) {
+        const long long rows = blk ? nl : el;
         for (int j = 0; j < m; ++j) {
           Step& s = pr.add();
           s.a_src = j == 0 ? A_TMA : A_ACT; s.a_map0 = 4;
@@ -582,12 +593,15 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         if (blk == 0) {
           s.flags |= EF_G16;
           s.g16 = ws->Ge[gc].p; s.g16_lo = ws->Ge[gc].lo; s.ga16 = ws->Ga.p; s.ga16_lo = ws->Ga.lo;
+          // G_e rows (< valid_in; none in the top layer, whose G_e is zero)
+          if (!ws->split && enext > 0) s.in_map = pr.in_map(ws->Ge[gc].p, enext, H);
         }
         s.scr_z = ws->scrZ[m].p; s.lo_off = ws->scrZ[m].lo;
         for (int j = m; j >= 1; --j) {
           Step& d = pr.add();
           d.a_src = A_ACT; d.K = H; d.b_map = W1; d.b_row0 = r1(li, (blk ? sl_nj(m) : sl_ej(m)) + j - 1);
           d.epi = EPI_DSILU; d.flags = blk == 1 ? EF_COLSUM_ALL : 0; d.scr_s = ws->scrS[j - 1].p; d.scr_z = ws->scrZ[j - 1].p; d.lo_off = ws->scrZ[j - 1].lo;
+          if (!ws->split) d.in_map = pr.in_map(ws->scrS[j - 1].p, rows, H);   // S'_{j-1} rows
           d.vec0 = 3 + (m - j);
         }
       };
@@ -627,6 +641,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         Step& a = pr.add();   // G_e^{l-1} = G_e' + dZ0 W0[e rows]^T
         a.a_src = A_ACT; a.K = H; a.b_map = W1; a.b_row0 = r1(li, sl_e1e(m));
         a.epi = EPI_ADD; a.flags = EF_G16; a.g16 = ws->Ge[gc].p; a.g16_lo = ws->Ge[gc].lo;
+        if (!ws->split) a.in_map = pr.in_map(ws->Ge[gc].p, el, H);   // G_e' rows
         a.g16_out = ws->Ge[gc ^ 1].p;
         run_prog(ws, "chain_edge_bwd", pr, (int)el, dp.src, dp.dst, true, st);
         colsum_reduce(ws, 0, li, grad_params, chain_grid(ws, (int)el), st, /*gamma_only=*/true);
