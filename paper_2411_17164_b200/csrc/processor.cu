@@ -299,7 +299,8 @@ static void wgrad(xmgn_workspace* ws, const BfBuf& a0, const BfBuf& a1, int a_wi
   const int NT = H >= 256 ? 256 : H;
   const int tiles = (Hin / 128 + (p.ones_tile ? 1 : 0)) * (H / NT);
   const int chunks = (int)((rows + 63) / 64);
-  int S = (2 * ws->sms + tiles - 1) / tiles;
+  // one wave: every CTA holds a 1-CTA/SM smem ring, so tiles x S <= SMs (no tail wave)
+  int S = ws->sms / tiles;
   if (S > chunks) S = chunks;
   if (S > ws->part_splits) S = ws->part_splits;
   if (S < 1) S = 1;
