@@ -147,8 +147,12 @@ def scope_work(info, H_=H, L_=L, m=M_HID):
         add("chain_proj", 0, 2 * 2 * H2 * npv)                      # recompute P in bwd
         add("chain_projbwd", 2 * 2 * H2 * npv)
         add("wgrad", 2 * ((2 + m) * H2 * nl + (1 + m) * H2 * el + 2 * H2 * npv))
-    agg_bytes = sum(4 * H_ * e_at(l) + 2 * H_ * n_at(l) for l in range(1, L_ + 1))
-    return w, agg_bytes
+    agg_bytes = sum(2 * H_ * e_at(l) + 2 * H_ * n_at(l) for l in range(1, L_ + 1))   # 16-bit edge rows in, 16-bit a out
+    rows = {"chain_edge_bwd": sum(e_at(l) for l in range(1, L_ + 1)),
+            "chain_edge_fwd": sum(e_at(l) for l in range(1, L_ + 1)),
+            "chain_node_bwd": sum(n_at(l) for l in range(1, L_ + 1)),
+            "chain_node_fwd": sum(n_at(l) for l in range(1, L_ + 1))}
+    return w, agg_bytes, rows
 
 
 def main():
@@ -243,9 +247,12 @@ def main():
     # ---- roofline of the dominant kernel scope (this rank's live CUDA-event timings)
     work = {}
     agg_bytes = 0
+    scope_rows = {}
     for p in parts:
-        w, ab = scope_work(pr.info[p], Hc, Lc, M_HID)
+        w, ab, rws = scope_work(pr.info[p], Hc, Lc, M_HID)
         agg_bytes += ab
+        for k, v in rws.items():
+            scope_rows[k] = scope_rows.get(k, 0) + v
         for k, (a, e) in w.items():
             A, Ee = work.get(k, (0.0, 0.0))
             work[k] = (A + a, Ee + e)
@@ -263,10 +270,16 @@ def main():
             achieved = alg / per_launch_s / 1e12
             peak = pk.get("bf16_tflops_sustained", 1400.0)
             unit, bound, src = "TFLOP/s", "tensor", "measured sustained bf16 (fp16 same nominal rate)"
+        # DRAM traffic per launch: dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set
+        # full capture of this scope (profiles/ncu_traffic.json, bytes per row of that launch),
+        # scaled to this run's average rows per launch
         traffic = None
         tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tf):
-            traffic = json.load(open(tf)).get(dom)
+            ent = json.load(open(tf)).get(dom)
+            rows = scope_rows.get(dom)
+            if ent and rows:
+                traffic = round(ent["bytes_per_row"] * rows * args.steps / n_launch)
         roof = {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
                 "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom, "peak_source": src,
                 "launches": n_launch, "avg_launch_ms": round(tot_ms / n_launch, 4),
