@@ -128,7 +128,37 @@ __global__ void __launch_bounds__(256) k_segsum(const int* __restrict__ off, con
 #pragma unroll
       for (int t = 0; t < 8; ++t) acc[v][t] = 0.f;
     const int k0 = off[i], k1 = off[i + 1];
-    for (int k = k0; k < k1; ++k) {
+    int k = k0;
+    if (!dz_lo) {
+      // batches of B edges: all B x V row-chunk loads are issued before any is summed
+      // (memory-level parallelism); the sums still run in CSR order
+      constexpr int B = 4;
+      for (; k + B <= k1; k += B) {
+        uint4 u[B][V];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          const int rk = rev[k + b];
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const int ch = lane + 32 * v;
+            const bool srcpart = ch < H / 8;
+            const int kk = srcpart ? rk : k + b;
+            const int c8 = srcpart ? ch : ch - H / 8;
+            u[b][v] = kk < e_act ? __ldg(reinterpret_cast<const uint4*>(dz + (size_t)kk * H) + c8) : make_uint4(0, 0, 0, 0);
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            float x[8];
+            unpack8<F16>(u[b][v], x);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[v][t] += x[t];
+          }
+      }
+    }
+    for (; k < k1; ++k) {
       const int rk = rev[k];
 #pragma unroll
       for (int v = 0; v < V; ++v) {
