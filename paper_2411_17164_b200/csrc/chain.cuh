@@ -90,6 +90,9 @@ struct Step {
   // bulk-loaded by TMA into the ACT tile once the accumulator is ready (ACT is dead then:
   // the step's MMAs have read it); map slot, -1 = read rows from global instead
   int in_map;
+  // EPI_SILU + EF_GATHER_P: the P[src] rows are TMA-gathered (tile::gather4) into ACT at
+  // accumulator-ready; map over P with 1-row boxes of 64 columns (-1 = row loads)
+  int gsrc_map;
 };
 
 constexpr int MAX_STEPS = 8;
@@ -819,6 +822,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
             mbar_wait(acc_full, g & 1);
             tc_fence_after();
             if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 2] = clock64();
+            if (st.gsrc_map >= 0) {
+              // P[src] rows of this warp's 32 tile rows, this column group's boxes: lane j
+              // issues box first + j for each group of 4 rows (src ids by shuffle)
+              if (threadIdx.x == 128)
+                for (int b = 0; b < H / 64; ++b) mbar_expect_tx(&in_full[b], 128 * 128);
+              const bool owner = (cb & 63) == 0;                  // narrow groups share a box
+              const int first = cb >> 6, nb = HC >= 64 ? HC / 64 : 1;
+#pragma unroll 1
+              for (int gi = 0; gi < 8; ++gi) {
+                const int s0 = __shfl_sync(0xffffffffu, src, 4 * gi), s1 = __shfl_sync(0xffffffffu, src, 4 * gi + 1);
+                const int s2 = __shfl_sync(0xffffffffu, src, 4 * gi + 2), s3 = __shfl_sync(0xffffffffu, src, 4 * gi + 3);
+                if (owner && lane < nb) {
+                  const int b = first + lane;
+                  tma_gather4(act + b * (128 * 128) + (q * 32 + 4 * gi) * 128, &p.maps[st.gsrc_map], &in_full[b], b * 64,
+                              s0, s1, s2, s3);
+                }
+              }
+            }
             if (st.in_map >= 0 && threadIdx.x == 128) {
               // the step's MMAs have read ACT: bulk-load the row input over it, in the order
               // the column groups consume the 64-column boxes
@@ -861,7 +882,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
               wrote_act = true;
             }
           }
-          if (st.in_map >= 0) ++nin;
+          if (st.in_map >= 0 || st.gsrc_map >= 0) ++nin;
         }
         tc_fence_before();
         if (wrote_act) fence_proxy_async_smem();

@@ -227,12 +227,14 @@ __device__ __forceinline__ void op_silu(const Epi& e, const Step& st, Wait wait)
   const __nv_bfloat16* pd = st.gather16 + (size_t)e.dst * 2 * H + H + e.cb;
   __nv_bfloat16* oa = st.scr_a + (size_t)e.r * H + e.cb;
   __nv_bfloat16* os = st.scr_s + (size_t)e.r * H + e.cb;
+  const bool tsrc = gp && st.gsrc_map >= 0;   // P[src] rows arrive in ACT by TMA gather
   uint32_t s0[8], d0[8], s1[8], d1[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) s0[i] = d0[i] = s1[i] = d1[i] = 0u;
   if (gp) {
-    ld16(ps, s0); ld16(pd, d0);
-    ld16(ps + 16, s1); ld16(pd + 16, d1);
+    if (!tsrc) { ld16(ps, s0); ld16(ps + 16, s1); }
+    ld16(pd, d0);
+    ld16(pd + 16, d1);
   }
   wait();
   uint32_t ta[16];
@@ -241,9 +243,19 @@ __device__ __forceinline__ void op_silu(const Epi& e, const Step& st, Wait wait)
     float x[16];
     lds16(e.sb + cc * 16, x);
     if (gp) {
-      add16<F16>(gs, x);
+      if (tsrc) {
+        float t[16];
+        in16<F16>(e, e.cb + cc * 16, t);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[i] += t[i];
+      } else {
+        add16<F16>(gs, x);
+      }
       add16<F16>(gd, x);
-      if (cc + 2 < NC) { ld16(ps + (cc + 2) * 16, gs); ld16(pd + (cc + 2) * 16, gd); }
+      if (cc + 2 < NC) {
+        if (!tsrc) ld16(ps + (cc + 2) * 16, gs);
+        ld16(pd + (cc + 2) * 16, gd);
+      }
     }
     tmem_wait16(ta);
 #pragma unroll

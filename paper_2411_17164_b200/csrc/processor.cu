@@ -163,7 +163,14 @@ struct Prog {
     std::memset(&s, 0, sizeof(s));
     s.a_map1 = -1;
     s.in_map = -1;
+    s.gsrc_map = -1;
     return s;
+  }
+  // TMA gather source over P [rows][2H] 16-bit: 1-row boxes of 64 columns
+  int gather_map(const bf16* base, long long rows, int width) {
+    if (next_map >= MAX_MAPS) throw Fail{set_error(XMGN_ESTATE, "internal: out of tensor-map slots")};
+    p.maps[next_map] = tmap_bf16(base, width, (uint64_t)(rows > 0 ? rows : 1), width, 64, 1);
+    return next_map++;
   }
   // TMA source of an epilogue row input: 16-bit rows [0, rows) x H, rows > 0 (rows beyond read zero)
   int in_map(const bf16* base, long long rows, int H) {
@@ -485,7 +492,10 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
           s.a_src = j == 0 ? A_TMA : A_ACT; s.a_map0 = 4; s.K = H;
           s.b_map = W1; s.b_row0 = r1(li, j == 0 ? SL_E1T : SL_EJT + j - 1);
           s.epi = EPI_SILU; s.bias = params + Ly.b(li, 0, j);
-          if (j == 0) { s.flags |= EF_GATHER_P; s.gather16 = ws->P.p; s.gather16_lo = ws->P.lo; }
+          if (j == 0) {
+            s.flags |= EF_GATHER_P; s.gather16 = ws->P.p; s.gather16_lo = ws->P.lo;
+            if (!ws->split) s.gsrc_map = pr.gather_map(ws->P.p, P.n_local, 2 * H);
+          }
         }
         // e^l = e^{l-1} + LN(..): the edge stream itself is 16-bit (checkpoint = next operand)
         Step& s = pr.add();
@@ -582,7 +592,10 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
           s.epi = EPI_SILU; s.bias = params + Ly.b(li, blk, j);
           s.flags = EF_STORE_A | EF_STORE_S;
           s.scr_a = ws->scrA[j].p; s.scr_s = ws->scrS[j].p; s.lo_off = ws->scrA[j].lo;
-          if (j == 0 && blk == 0) { s.flags |= EF_GATHER_P; s.gather16 = ws->P.p; s.gather16_lo = ws->P.lo; }
+          if (j == 0 && blk == 0) {
+            s.flags |= EF_GATHER_P; s.gather16 = ws->P.p; s.gather16_lo = ws->P.lo;
+            if (!ws->split) s.gsrc_map = pr.gather_map(ws->P.p, P.n_local, 2 * H);
+          }
         }
         Step& s = pr.add();
         s.a_src = A_ACT; s.K = H; s.b_map = W1; s.b_row0 = r1(li, (blk ? sl_njt(m) : SL_EJT) + m - 1);
