@@ -93,10 +93,13 @@ struct Step {
   // EPI_SILU + EF_GATHER_P: the P[src] rows are TMA-gathered (tile::gather4) into ACT at
   // accumulator-ready; map over P with 1-row boxes of 64 columns (-1 = row loads)
   int gsrc_map;
+  // outputs equal to the ACT tile this epilogue writes (A_j, dZ_j scratch) leave by TMA
+  // bulk stores straight from ACT (map slot, -1 = row stores)
+  int st_map;
 };
 
 constexpr int MAX_STEPS = 8;
-constexpr int MAX_MAPS = 16;
+constexpr int MAX_MAPS = 24;
 constexpr int NV_MAX = 5;  // column-sum vectors per kernel
 // Epilogue: EW warps per TMEM lane quadrant, each owning H/EW columns of its 32
 // rows (row statistics are exchanged through shared memory).  The 16-bit modes
@@ -545,6 +548,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
     const uint32_t acc_empty_l = mapa_shared(smem_u32(acc_empty), 0);
     const uint32_t act_full_l = mapa_shared(smem_u32(act_full), 0);
     int g = 0, nin = 0;   // nin: steps whose input came through in_full (its phase)
+    // TMA stores of ACT boxes: with HC >= 64 each column group stores its own boxes
+    // (barrier 9 + eg over its 4 warps, issuer = lane 0 of its quadrant-0 warp); with
+    // narrower groups all epilogue warps share barrier 9 and thread 128 issues.
+    constexpr bool GROUP_STORES = HC >= 64;
+    const int sbar = GROUP_STORES ? 9 + eg : 9;
+    constexpr int SBAR_THREADS = GROUP_STORES ? 128 : NEPI;
+    const bool issuer = GROUP_STORES ? (q == 0 && lane == 0) : (threadIdx.x == 128);
+    bool st_pending = false;   // TMA stores out of ACT may still be reading it
     for (int tile = cid; tile < n_tiles; tile += ncl) {
       const int r = tile * 256 + (int)rank * 128 + trow;
       const bool valid = r < p.M;
@@ -822,6 +833,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
             mbar_wait(acc_full, g & 1);
             tc_fence_after();
             if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 2] = clock64();
+            if (st_pending) {   // the previous step's stores must have read ACT before anything rewrites it
+              if (issuer) bulk_wait_read0();
+              named_bar(13, NEPI);
+              st_pending = false;
+            }
             if (st.gsrc_map >= 0) {
               // P[src] rows of this warp's 32 tile rows, this column group's boxes: lane j
               // issues box first + j for each group of 4 rows (src ids by shuffle)
@@ -883,6 +899,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
             }
           }
           if (st.in_map >= 0 || st.gsrc_map >= 0) ++nin;
+          if (st.st_map >= 0) {
+            // this thread-set's ACT boxes -> global rows [row0, row0 + 128) by TMA
+            fence_proxy_async_smem();
+            named_bar(sbar, SBAR_THREADS);
+            if (issuer) {
+              const int row0 = tile * 256 + (int)rank * 128;
+              const int b0 = GROUP_STORES ? cb / 64 : 0, nb = GROUP_STORES ? HC / 64 : H / 64;
+              for (int b = b0; b < b0 + nb; ++b) tma_store_2d(&p.maps[st.st_map], act + b * (128 * 128), b * 64, row0);
+              bulk_commit();
+            }
+            st_pending = true;
+          }
+          // the next step refills the A ring (aliases ACT): drain before arriving
+          {
+            const Step& nx = p.steps[s + 1 < p.n_steps ? s + 1 : 0];
+            if (st_pending && nx.a_src == A_TMA && (nx.ctl & CTL_NEED_ACT_FREE)) {
+              if (issuer) bulk_wait_read0();
+              st_pending = false;
+            }
+          }
         }
         tc_fence_before();
         if (wrote_act) fence_proxy_async_smem();

@@ -222,7 +222,8 @@ __device__ __forceinline__ void ln_stats16(const Epi& e, float eps, RowSum row_s
 template <int H, int NC, bool F16, class Wait>
 __device__ __forceinline__ void op_silu(const Epi& e, const Step& st, Wait wait) {
   const bool gp = (st.flags & EF_GATHER_P) != 0;
-  const bool sa = e.valid && (st.flags & EF_STORE_A) != 0, ss = (st.flags & EF_STORE_S) != 0;
+  // A leaves by TMA from ACT when st_map is set, else by row stores
+  const bool sa = e.valid && (st.flags & EF_STORE_A) != 0 && st.st_map < 0, ss = (st.flags & EF_STORE_S) != 0;
   const __nv_bfloat16* ps = st.gather16 + (size_t)e.src * 2 * H + e.cb;
   const __nv_bfloat16* pd = st.gather16 + (size_t)e.dst * 2 * H + H + e.cb;
   __nv_bfloat16* oa = st.scr_a + (size_t)e.r * H + e.cb;
@@ -422,7 +423,7 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
 #pragma unroll
     for (int i = 0; i < 16; ++i) dy[i] = e.valid ? rstd * (dy[i] * gm[i] - s1 - xh[i] * s2) : 0.f;
     sts_tile16<F16>(e.act, e.trow, c0, dy);
-    if (e.valid) st16<F16>(zp + cc * 16, dy);
+    if (e.valid && st.st_map < 0) st16<F16>(zp + cc * 16, dy);
     if (csall) colsum16_add<H>(e, 2, c0, dy);        // db_{m+1}
   }
 }
@@ -496,7 +497,7 @@ __device__ __forceinline__ void op_ln_bwd32(const Epi& e, const Step& st, Wait w
 #pragma unroll
     for (int i = 0; i < 16; ++i) dy[i] = e.valid ? rstd * (dy[i] * gm[i] - s1 - xh[i] * s2) : 0.f;
     sts_tile16<F16>(e.act, e.trow, c0, dy);
-    if (e.valid) st16<F16>(zp + cc * 16, dy);
+    if (e.valid && st.st_map < 0) st16<F16>(zp + cc * 16, dy);
     if (csall) colsum16_add<H>(e, 2, c0, dy);
   };
 #pragma unroll 1
@@ -531,7 +532,7 @@ __device__ __forceinline__ void op_dsilu(const Epi& e, const Step& st, Wait wait
     for (int i = 0; i < 16; ++i) x[i] *= __uint_as_float(ta[i]);
     if (cc + 1 < NC) tmem_ld16_async(e.tl + (cc + 1) * 16, ta);
     sts_tile16<F16>(e.act, e.trow, c0, x);
-    if (e.valid) st16<F16>(zp + cc * 16, x);
+    if (e.valid && st.st_map < 0) st16<F16>(zp + cc * 16, x);
     if (csall) colsum16_add<H>(e, st.vec0, c0, x);
   };
 #pragma unroll 1

@@ -164,6 +164,7 @@ struct Prog {
     s.a_map1 = -1;
     s.in_map = -1;
     s.gsrc_map = -1;
+    s.st_map = -1;
     return s;
   }
   // TMA gather source over P [rows][2H] 16-bit: 1-row boxes of 64 columns
@@ -504,7 +505,7 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
         s.gamma = params + Ly.gamma(li, 0); s.beta = params + Ly.beta(li, 0);
         s.flags = EF_RES16 | EF_STORE_BF;
         s.res16 = eck_prev.p; s.res16_lo = eck_prev.lo;
-        if (!ws->split) s.in_map = pr.in_map(eck_prev.p, el, H);   // residual e^{l-1} rows
+        if (!ws->split && el > 0) s.in_map = pr.in_map(eck_prev.p, el, H);   // residual e^{l-1} rows
         s.bf_out = eck_next.p; s.bf_lo = eck_next.lo;
         run_prog(ws, "chain_edge_fwd", pr, (int)el, dp.src, dp.dst, false, st);
       }
@@ -592,6 +593,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
           s.epi = EPI_SILU; s.bias = params + Ly.b(li, blk, j);
           s.flags = EF_STORE_A | EF_STORE_S;
           s.scr_a = ws->scrA[j].p; s.scr_s = ws->scrS[j].p; s.lo_off = ws->scrA[j].lo;
+          if (!ws->split && rows > 0) s.st_map = pr.in_map(ws->scrA[j].p, rows, H);   // A_j = the ACT tile, TMA-stored
           if (j == 0 && blk == 0) {
             s.flags |= EF_GATHER_P; s.gather16 = ws->P.p; s.gather16_lo = ws->P.lo;
             if (!ws->split) s.gsrc_map = pr.gather_map(ws->P.p, P.n_local, 2 * H);
@@ -611,11 +613,13 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
           if (!ws->split && enext > 0) s.in_map = pr.in_map(ws->Ge[gc].p, enext, H);
         }
         s.scr_z = ws->scrZ[m].p; s.lo_off = ws->scrZ[m].lo;
+        if (!ws->split && rows > 0) s.st_map = pr.in_map(ws->scrZ[m].p, rows, H);   // dZ_m = the ACT tile, TMA-stored
         for (int j = m; j >= 1; --j) {
           Step& d = pr.add();
           d.a_src = A_ACT; d.K = H; d.b_map = W1; d.b_row0 = r1(li, (blk ? sl_nj(m) : sl_ej(m)) + j - 1);
           d.epi = EPI_DSILU; d.flags = blk == 1 ? EF_COLSUM_ALL : 0; d.scr_s = ws->scrS[j - 1].p; d.scr_z = ws->scrZ[j - 1].p; d.lo_off = ws->scrZ[j - 1].lo;
-          if (!ws->split) d.in_map = pr.in_map(ws->scrS[j - 1].p, rows, H);   // S'_{j-1} rows
+          if (!ws->split && rows > 0) d.in_map = pr.in_map(ws->scrS[j - 1].p, rows, H);   // S'_{j-1} rows
+          if (!ws->split && rows > 0) d.st_map = pr.in_map(ws->scrZ[j - 1].p, rows, H);   // dZ_{j-1} = the ACT tile
           d.vec0 = 3 + (m - j);
         }
       };
@@ -655,7 +659,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         Step& a = pr.add();   // G_e^{l-1} = G_e' + dZ0 W0[e rows]^T
         a.a_src = A_ACT; a.K = H; a.b_map = W1; a.b_row0 = r1(li, sl_e1e(m));
         a.epi = EPI_ADD; a.flags = EF_G16; a.g16 = ws->Ge[gc].p; a.g16_lo = ws->Ge[gc].lo;
-        if (!ws->split) a.in_map = pr.in_map(ws->Ge[gc].p, el, H);   // G_e' rows
+        if (!ws->split && el > 0) a.in_map = pr.in_map(ws->Ge[gc].p, el, H);   // G_e' rows
         a.g16_out = ws->Ge[gc ^ 1].p;
         run_prog(ws, "chain_edge_bwd", pr, (int)el, dp.src, dp.dst, true, st);
         colsum_reduce(ws, 0, li, grad_params, chain_grid(ws, (int)el), st, /*gamma_only=*/true);
