@@ -409,7 +409,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
           const bool tma_a = st.a_src == A_TMA;
           if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) { mbar_wait(act_free, naf & 1); ++naf; }
           for (int kc = 0; kc < st.K / 64; ++kc) {
-            if (kc == 1 && p.trace && blockIdx.x == 0 && g < 64) p.trace[g * 8 + 7] = clock64();
             if (tma_a) {
               const int slot = ai % C::SA;
               if (ai >= C::SA) mbar_wait(&a_empty[slot], ((ai / C::SA) - 1) & 1);
@@ -451,6 +450,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
           // the previous epilogue must be done (it may still read its input out of ACT)
           // before ACT can become A-ring space again
           if (g > 0) mbar_wait(acc_empty, (g - 1) & 1);
+          if (p.trace && blockIdx.x == 0 && g < 64 && lane_id() == 0) p.trace[g * 8 + 7] = clock64();
           if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) {
             // let every issued MMA (the ones reading ACT) retire, then hand both
             // CTAs' ACT tiles to their producers as A-ring space.
@@ -928,6 +928,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         // one release-arrive per CTA after the epilogue warps synchronise: only this
         // warp's global stores sit in front of its release fence
         named_bar(8, NEPI);
+        if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 4] = clock64();
         if (threadIdx.x == 128) {
           mbar_arrive_cluster(acc_empty_l);
           if (wrote_act) mbar_arrive_cluster(act_full_l);

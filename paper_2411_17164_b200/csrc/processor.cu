@@ -253,7 +253,7 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
     cudaStreamSynchronize(st);
     FILE* f = fopen("gpurun_out/trace.txt", "w");
     if (f) {
-      fprintf(f, "# %s M=%d steps=%d: g, mma_start, mma_issued, epi_start, ln_stats, lnbwd_passA, epi_end_w4, epi_end_w8, prod_kc1\n",
+      fprintf(f, "# %s M=%d steps=%d: g, mma_start, mma_issued, epi_start, (split: ln_stats), epi_all_done, epi_end_w4, epi_end_w8, mma_after_acc_empty\n",
               name, M, pr.n);
       const unsigned long long t0 = h[0];
       for (int g = 0; g < 64; ++g) {
