@@ -300,17 +300,40 @@ def main():
         host = {}
         for p in parts:
             host[p] = [x.cpu().pin_memory() for x in inputs[p]]
-        dev_in = inputs   # the user's device staging buffers, refilled from host every step
         grad_host = torch.empty(pr.n_params, dtype=torch.float32).pin_memory()
         bi = sum(x.numel() * 4 for p in parts for x in host[p])
         bo = grad_host.numel() * 4
+        # two device staging sets (sized for the largest partition of this rank): partition
+        # i+1's inputs are copied host->device on a copy stream while partition i computes
+        del inputs
+        torch.cuda.empty_cache()
+        shapes = [max(host[p][j].shape[0] for p in parts) for j in range(3)]
+        stage = [[torch.empty((shapes[j], Hc), dtype=torch.float32, device=dev) for j in range(3)] for _ in range(2)]
+        cstream = torch.cuda.Stream(device=dev)
+        ready = [torch.cuda.Event() for _ in range(2)]
+        free = [torch.cuda.Event() for _ in range(2)]
+        for f in free:
+            f.record(stream)
 
         def e2e_step():
-            for p in parts:
-                for d_, h_ in zip(dev_in[p], host[p]):
-                    d_.copy_(h_, non_blocking=True)
+            def h2d(i):
+                b = i % 2
+                cstream.wait_event(free[b])
+                with torch.cuda.stream(cstream):
+                    for j in range(3):
+                        stage[b][j][:host[parts[i]][j].shape[0]].copy_(host[parts[i]][j], non_blocking=True)
+                ready[b].record(cstream)
             grad.zero_()
-            pr.step(params, grad, dev_in, stream)
+            h2d(0)
+            for i, p in enumerate(parts):
+                b = i % 2
+                if i + 1 < len(parts):
+                    h2d(i + 1)
+                stream.wait_event(ready[b])
+                h0, e0, g = (stage[b][j][:host[p][j].shape[0]] for j in range(3))
+                pr.forward(p, params, h0, e0, stream)
+                pr.backward(p, params, g, grad, stream=stream)
+                free[b].record(stream)
             if comm is not None:
                 comm.grad_reduce(grad, stream)
             grad_host.copy_(grad, non_blocking=True)
@@ -319,6 +342,7 @@ def main():
         sync_all()
         k2 = max(1, min(args.steps, 2))
         ev0.record(stream)
+        cstream.wait_event(ev0)       # no copy of the timed steps starts before ev0
         for _ in range(k2):
             e2e_step()
         ev1.record(stream)
@@ -328,7 +352,8 @@ def main():
         if world > 1:
             dist.all_reduce(t3, op=dist.ReduceOp.MAX)
         e2e = {"value": E_global / (float(t3.item()) / 1e3), "unit": "edges/s", "h2d_bytes_per_step": bi,
-               "d2h_bytes_per_step": bo, "steps": k2}
+               "d2h_bytes_per_step": bo, "steps": k2,
+               "note": "pinned host inputs copied on a second stream, partition i+1 overlapping partition i"}
         del host
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1)
