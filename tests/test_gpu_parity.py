@@ -191,3 +191,34 @@ def test_cfg4_probe_forward():
     for pnode in np.random.default_rng(1).choice(N, 1, replace=False):
         o = oracle_probe(b, int(pnode), 512, 15, with_grad=False)
         assert np.abs(res["h"][pnode] - o["h"]).max() <= TAU[FP16] * rms
+
+
+def _hand_bundle(offsets, sources, owner, P, halo):
+    from xmgn_inputs import partition as part
+    offsets = np.asarray(offsets, np.int64)
+    sources = np.asarray(sources, np.int64)
+    return dict(offsets=offsets, sources=sources, owner=np.asarray(owner),
+                **part.partition_set(offsets, sources, np.asarray(owner), P, halo))
+
+
+@pytest.mark.parametrize("prec", [FP32, FP16])
+def test_degenerate_graphs(prec):
+    """Degenerate inputs: isolated nodes (empty in-neighbourhood: agg = 0),
+    fewer edges than one 128-row tile, and partitions whose halo-shrunk top layers have
+    no edges at all.  Path 0-1-2-3-4 plus isolated nodes 5 and 6, split into 3 partitions."""
+    # CSR by destination, sources ascending, symmetric
+    nbr = {0: [1], 1: [0, 2], 2: [1, 3], 3: [2, 4], 4: [3], 5: [], 6: []}
+    offsets = np.cumsum([0] + [len(nbr[i]) for i in range(7)])
+    sources = np.concatenate([nbr[i] for i in range(7)]).astype(np.int64)
+    b = _hand_bundle(offsets, sources, [0, 0, 1, 1, 2, 2, 2], 3, 2)
+    res = run_gpu(b, 128, 2, prec)
+    ref = oracle_full(b, 128, 2)
+    _check(res, ref, 128, 2, TAU[prec])
+
+
+def test_single_partial_tile_many_partitions():
+    """Every partition smaller than one CTA pair tile (256 rows), ragged everywhere."""
+    b = configs.custom((60, 180), k=4, P=6, halo=3)
+    res = run_gpu(b, 256, 3, FP16)
+    ref = oracle_full(b, 256, 3)
+    _check(res, ref, 256, 3, TAU[FP16])
