@@ -49,8 +49,9 @@ enum : int {
   EF_OUT16 = 256,      // EPI_STORE: write 16-bit bf_out (ld_out, col0) instead of fp32 f_out
   EF_COLSUM_ALL = 1024,  // EPI_LN_BWD / EPI_DSILU: also accumulate dbeta / db column sums here
                          // (else only dgamma; the bias sums come from the wgrad GEMMs)
-  EF_G16 = 512         // EPI_LN_BWD / EPI_ADD: the gradient stream is the 16-bit g16 (edge programs):
+  EF_G16 = 512,        // EPI_LN_BWD / EPI_ADD: the gradient stream is the 16-bit g16 (edge programs):
                        // LN_BWD writes dY = g16 (+ ga16[dst]) back into g16; ADD does g16 += acc
+  EF_DISCARD = 2048    // EPI_DSILU: this is the last read of S' -- drop its L2 lines afterwards
 };
 
 enum : int {
@@ -163,6 +164,11 @@ struct ChainCfg {
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ float sigmoid_fast(float v) {
   float t;
   asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * v));
@@ -450,7 +456,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
           // the previous epilogue must be done (it may still read its input out of ACT)
           // before ACT can become A-ring space again
           if (g > 0) mbar_wait(acc_empty, (g - 1) & 1);
-          if (p.trace && blockIdx.x == 0 && g < 64 && lane_id() == 0) p.trace[g * 8 + 7] = clock64();
+          if (p.trace && blockIdx.x == 0 && g < 64 && lane_id() == 0) p.trace[g * 8 + 7] = gtimer();
           if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) {
             // let every issued MMA (the ones reading ACT) retire, then hand both
             // CTAs' ACT tiles to their producers as A-ring space.
@@ -548,6 +554,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
     const uint32_t acc_empty_l = mapa_shared(smem_u32(acc_empty), 0);
     const uint32_t act_full_l = mapa_shared(smem_u32(act_full), 0);
     int g = 0, nin = 0;   // nin: steps whose input came through in_full (its phase)
+    const uint64_t pol_last = policy_evict_last();
     // TMA stores of ACT boxes: with HC >= 64 each column group stores its own boxes
     // (barrier 9 + eg over its 4 warps, issuer = lane 0 of its quadrant-0 warp); with
     // narrower groups all epilogue warps share barrier 9 and thread 128 issues.
@@ -712,7 +719,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
             }
             s1 = row_sum(s1) * (1.0f / H);
             s2 = row_sum(s2) * (1.0f / H);
-            if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 4] = clock64();
+            // hand-off timing in globaltimer ns (comparable across the pair): CTA 0 -> col 4, CTA 1 -> col 3
+        if (p.trace && blockIdx.x < 2 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 4 - (int)blockIdx.x] = gtimer();
 #pragma unroll 1
             for (int cc = 0; cc < NC; ++cc) {
               const int c0 = cb + cc * 32;
@@ -873,7 +881,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
           Epi e;
           e.act = act; e.tl = tl; e.trow = trow; e.cb = cb; e.r = r; e.src = src; e.dst = dst; e.valid = valid;
           e.sb = prm + cb; e.sg = prm + H + cb; e.sbt = prm + 2 * H + cb; e.colsum = colsum_base; e.eps = p.eps;
-          e.in_full = in_full; e.in_par = nin & 1;
+          e.in_full = in_full; e.in_par = nin & 1; e.pol_last = pol_last;
           constexpr int NC16 = HC / 16;
           const int op = st.epi;
           if (op == EPI_SILU) {
@@ -928,7 +936,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         // one release-arrive per CTA after the epilogue warps synchronise: only this
         // warp's global stores sit in front of its release fence
         named_bar(8, NEPI);
-        if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 4] = clock64();
+        // hand-off timing in globaltimer ns (comparable across the pair): CTA 0 -> col 4, CTA 1 -> col 3
+        if (p.trace && blockIdx.x < 2 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 4 - (int)blockIdx.x] = gtimer();
         if (threadIdx.x == 128) {
           mbar_arrive_cluster(acc_empty_l);
           if (wrote_act) mbar_arrive_cluster(act_full_l);

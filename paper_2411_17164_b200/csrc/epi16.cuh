@@ -167,6 +167,7 @@ struct Epi {
   float eps;
   uint64_t* in_full; // [H/64] mbarriers: TMA-loaded input boxes in ACT (Step::in_map)
   uint32_t in_par;   // their phase parity for this step
+  uint64_t pol_last; // L2 evict_last policy (in-kernel scratch)
 };
 
 // 16 values of this row's TMA-loaded input (ACT, columns c0 .. c0+15), after the box landed
@@ -265,7 +266,11 @@ __device__ __forceinline__ void op_silu(const Epi& e, const Step& st, Wait wait)
     if (ss) {
       float dv[16];
       silu_grad16<F16>(x, dv);
-      if (e.valid) st16<F16>(os + cc * 16, dv);
+      if (e.valid) {                    // S': read again in this kernel -> keep in L2
+        uint32_t h[8];
+        pack16x16<F16>(dv, h);
+        stg256_pol(os + cc * 16, h, e.pol_last);
+      }
     } else {
       silu16<F16>(x);
     }
@@ -539,6 +544,10 @@ __device__ __forceinline__ void op_dsilu(const Epi& e, const Step& st, Wait wait
   for (int cc = 0; cc < NC; cc += 2) {
     body(cc, q0);
     body(cc + 1, q1);
+  }
+  if (e.valid && (st.flags & EF_DISCARD)) {   // last read of S' (consumed above): drop its lines
+#pragma unroll
+    for (int i = 0; i < NC * 16 * 2 / 128; ++i) discard_l2_line(reinterpret_cast<const uint8_t*>(sp) + 128 * i);
   }
 }
 

@@ -617,7 +617,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         for (int j = m; j >= 1; --j) {
           Step& d = pr.add();
           d.a_src = A_ACT; d.K = H; d.b_map = W1; d.b_row0 = r1(li, (blk ? sl_nj(m) : sl_ej(m)) + j - 1);
-          d.epi = EPI_DSILU; d.flags = blk == 1 ? EF_COLSUM_ALL : 0; d.scr_s = ws->scrS[j - 1].p; d.scr_z = ws->scrZ[j - 1].p; d.lo_off = ws->scrZ[j - 1].lo;
+          d.epi = EPI_DSILU; d.flags = (blk == 1 ? EF_COLSUM_ALL : 0) | EF_DISCARD; d.scr_s = ws->scrS[j - 1].p; d.scr_z = ws->scrZ[j - 1].p; d.lo_off = ws->scrZ[j - 1].lo;
           if (!ws->split && rows > 0) d.in_map = pr.in_map(ws->scrS[j - 1].p, rows, H);   // S'_{j-1} rows
           if (!ws->split && rows > 0) d.st_map = pr.in_map(ws->scrZ[j - 1].p, rows, H);   // dZ_{j-1} = the ACT tile
           d.vec0 = 3 + (m - j);

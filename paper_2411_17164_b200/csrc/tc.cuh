@@ -277,6 +277,24 @@ __device__ __forceinline__ void stg256(void* p, const uint32_t* r) {
                : "memory");
 }
 
+// L2 eviction-priority policy and hinted 256-bit store.  Scratch produced and consumed
+// inside one chain kernel (S'_j) is written evict_last and dropped with
+// discard.global.L2 after its last read, so it need not reach HBM.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void stg256_pol(void* p, const uint32_t* r, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "l"(pol)
+               : "memory");
+}
+// drop one 128-byte L2 line without writing it back (its contents become undefined)
+__device__ __forceinline__ void discard_l2_line(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
 // Asynchronous variant: issue the TMEM load, consume only after tmem_wait32(r)
 // (the wait takes the registers as in/out operands so no use can be hoisted).
 __device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t* r) {
