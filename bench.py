@@ -278,7 +278,7 @@ def main():
         if os.path.exists(tf):
             ent = json.load(open(tf)).get(dom)
             rows = scope_rows.get(dom)
-            if ent and rows:
+            if ent and rows and ent.get("config", args.config) == args.config:
                 traffic = round(ent["bytes_per_row"] * rows * args.steps / n_launch)
         roof = {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
                 "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom, "peak_source": src,
