@@ -144,7 +144,6 @@ def scope_work(info, H_=H, L_=L, m=M_HID):
         fw_e, fw_n = 2 * (1 + m) * H2 * el, 2 * (2 + m) * H2 * nl
         add("chain_node_bwd", 2 * (m + 2) * H2 * nl, fw_n + 2 * (m + 2) * H2 * nl)
         add("chain_edge_bwd", 2 * (m + 1) * H2 * el, fw_e + 2 * (m + 1) * H2 * el)
-        add("chain_proj", 0, 2 * 2 * H2 * npv)                      # recompute P in bwd
         add("chain_projbwd", 2 * 2 * H2 * npv)
         add("wgrad", 2 * ((2 + m) * H2 * nl + (1 + m) * H2 * el + 2 * H2 * npv))
     agg_bytes = sum(2 * H_ * e_at(l) + 2 * H_ * n_at(l) for l in range(1, L_ + 1))   # 16-bit edge rows in, 16-bit a out

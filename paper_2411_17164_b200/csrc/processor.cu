@@ -53,7 +53,7 @@ struct xmgn_workspace {
   // checkpoints (per layer) and live streams
   xmgn::BfBuf e_ck, h_ck, a_ck;   // e_ck [L+1][Emax][H] (the 16-bit edge stream), h_ck / a_ck [L][Nmax][H]
   float *h_buf[2] = {nullptr, nullptr};
-  xmgn::BfBuf P;                  // node pre-projection [Nmax][2H], 16-bit
+  xmgn::BfBuf P;                  // node pre-projections, one per layer [L][Nmax][2H], 16-bit (kept for the bwd)
   // backward
   float* Gh = nullptr;            // dL/dh (FP32, node level)
   xmgn::BfBuf Ge[2], Ga;          // dL/de (16-bit edge stream, ping-pong), dL/da (16-bit)
@@ -410,7 +410,7 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
       ws->h_ck = bfalloc(ws, (size_t)L * NH);
       ws->a_ck = bfalloc(ws, (size_t)L * NH);
       for (int i = 0; i < 2; ++i) ws->h_buf[i] = (float*)dalloc(ws, NH * 4);
-      ws->P = bfalloc(ws, 2 * NH);
+      ws->P = bfalloc(ws, (size_t)L * 2 * NH);
       ws->Ge[0] = bfalloc(ws, EH);
       ws->Ge[1] = bfalloc(ws, EH);
       ws->Gh = (float*)dalloc(ws, NH * 4);
@@ -476,6 +476,7 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
       }
       run_prog(ws, "chain_proj", pr, (int)n0, nullptr, nullptr, false, st);
     }
+    auto Pl = [&](int li) { return ws->P.p + (long long)li * 2 * NH; };   // P of layer li + 1
     int cur = 0;
     for (int l = 1; l <= L; ++l) {
       const int li = l - 1;
@@ -494,8 +495,8 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
           s.b_map = W1; s.b_row0 = r1(li, j == 0 ? SL_E1T : SL_EJT + j - 1);
           s.epi = EPI_SILU; s.bias = params + Ly.b(li, 0, j);
           if (j == 0) {
-            s.flags |= EF_GATHER_P; s.gather16 = ws->P.p; s.gather16_lo = ws->P.lo;
-            if (!ws->split) s.gsrc_map = pr.gather_map(ws->P.p, P.n_local, 2 * H);
+            s.flags |= EF_GATHER_P; s.gather16 = Pl(li); s.gather16_lo = ws->P.lo;
+            if (!ws->split) s.gsrc_map = pr.gather_map(Pl(li), P.n_local, 2 * H);
           }
         }
         // e^l = e^{l-1} + LN(..): the edge stream itself is 16-bit (checkpoint = next operand)
@@ -536,7 +537,7 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
           for (int half = 0; half < 2; ++half) {
             Step& q = pr.add();
             q.a_src = A_ACT; q.K = H; q.b_map = W1; q.b_row0 = r1(l, half ? SL_PDT : SL_PST);
-            q.epi = EPI_STORE; q.flags = EF_OUT16; q.bf_out = ws->P.p; q.bf_lo = ws->P.lo; q.ld_out = 2 * H;
+            q.epi = EPI_STORE; q.flags = EF_OUT16; q.bf_out = Pl(l); q.bf_lo = ws->P.lo; q.ld_out = 2 * H;
             q.col0 = half * H;
           }
         }
@@ -563,6 +564,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
     const DPart& dp = ws->dparts[part];
     const int H = ws->H, L = ws->L, m = ws->m;
     const long long NH = ws->Nmax * (long long)H, EH = ws->Emax * (long long)H;
+    auto Pl = [&](int li) { return ws->P.p + (long long)li * 2 * NH; };   // the forward's P of layer li + 1
     Layout Ly{H, L, m};
     const int W1 = 0, W2 = 2;
     auto r1 = [&](int l, int slot) { return (l * ws->S1 + slot) * H; };
@@ -595,8 +597,8 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
           s.scr_a = ws->scrA[j].p; s.scr_s = ws->scrS[j].p; s.lo_off = ws->scrA[j].lo;
           if (!ws->split && rows > 0) s.st_map = pr.in_map(ws->scrA[j].p, rows, H);   // A_j = the ACT tile, TMA-stored
           if (j == 0 && blk == 0) {
-            s.flags |= EF_GATHER_P; s.gather16 = ws->P.p; s.gather16_lo = ws->P.lo;
-            if (!ws->split) s.gsrc_map = pr.gather_map(ws->P.p, P.n_local, 2 * H);
+            s.flags |= EF_GATHER_P; s.gather16 = Pl(li); s.gather16_lo = ws->P.lo;
+            if (!ws->split) s.gsrc_map = pr.gather_map(Pl(li), P.n_local, 2 * H);
           }
         }
         Step& s = pr.add();
@@ -640,18 +642,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         for (int j = 1; j <= m; ++j)
           wgrad(ws, ws->scrA[j - 1], none, H, H / 128, ws->scrZ[j], H, 0, nl, H, grad_params, Ly.W(li, 1, j), st);
       }
-      {  // recompute P for layer l from h^{l-1}
-        Prog pr;
-        set_a(ws, pr, 4, hck, nprev, H);
-        for (int half = 0; half < 2; ++half) {
-          Step& s = pr.add();
-          s.a_src = A_TMA; s.a_map0 = 4; s.K = H;
-          s.b_map = W1; s.b_row0 = r1(li, half ? SL_PDT : SL_PST);
-          s.epi = EPI_STORE; s.flags = EF_OUT16; s.bf_out = ws->P.p; s.bf_lo = ws->P.lo; s.ld_out = 2 * H;
-          s.col0 = half * H;
-        }
-        run_prog(ws, "chain_proj", pr, (int)nprev, nullptr, nullptr, false, st);
-      }
+      // P for layer l: the forward's checkpoint (no recompute)
       {  // edge block backward
         Prog pr;
         set_a(ws, pr, 4, eck, el, H);
