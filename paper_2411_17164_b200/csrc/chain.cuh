@@ -109,9 +109,6 @@ constexpr int NV_MAX = 5;  // column-sum vectors per kernel
 #ifndef XMGN_EPI_GROUPS
 #define XMGN_EPI_GROUPS 4
 #endif
-#ifndef XMGN_EPI_SINGLE_ARRIVE
-#define XMGN_EPI_SINGLE_ARRIVE 1
-#endif
 template <bool SPLIT>
 struct EpiShape {
   static constexpr int EW = SPLIT ? 2 : XMGN_EPI_GROUPS;
@@ -372,7 +369,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
   const int cid = (int)cluster_id_x(), ncl = (int)n_clusters_x();
   const int n_tiles = (p.M + 255) / 256;     // pair tiles of 256 rows (128 per CTA)
   constexpr int EPI_WARPS = NEPI / 32;
-  constexpr int EPI_ARRIVALS = XMGN_EPI_SINGLE_ARRIVE ? 1 : EPI_WARPS;
+  constexpr int EPI_ARRIVALS = 1;   // warp 3, once per CTA and step
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::SA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < C::SB; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
@@ -518,6 +515,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         }
       }
     }
+  } else if (w == 3) {
+    // ============================ step hand-off: joins the epilogue's end-of-step barrier and
+    // arrives on the leader's acc_empty / act_full.  A release at cluster scope waits for
+    // the arriving thread's own outstanding global stores (MEMBAR.GPU); this warp has none,
+    // the epilogue warps (which store) would stall the hand-off by ~2 us per step.
+    const uint32_t acc_empty_l = mapa_shared(smem_u32(acc_empty), 0);
+    const uint32_t act_full_l = mapa_shared(smem_u32(act_full), 0);
+    int g = 0;
+    for (int tile = cid; tile < n_tiles; tile += ncl) {
+      for (int s = 0; s < p.n_steps; ++s, ++g) {
+        const Step& st = p.steps[s];
+        const bool wa = st.epi == EPI_SILU || st.epi == EPI_LN_BWD || st.epi == EPI_DSILU ||
+                        (st.epi == EPI_LN_FWD && (st.flags & EF_WRITE_ACT));
+        named_bar(8, NEPI + 32);
+        if (p.trace && blockIdx.x < 2 && g < 64 && lane_id() == 0) p.trace[g * 8 + 4 - (int)blockIdx.x] = gtimer();
+        if (lane_id() == 0) {
+          mbar_arrive_cluster(acc_empty_l);
+          if (wa) mbar_arrive_cluster(act_full_l);
+        }
+        __syncwarp();
+      }
+    }
   }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(ES::EPI_REGS) : "memory");
@@ -551,8 +570,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
       float* dstp = colsum_base + (size_t)vec * H + c0 + lane;
       *dstp += cs;
     };
-    const uint32_t acc_empty_l = mapa_shared(smem_u32(acc_empty), 0);
-    const uint32_t act_full_l = mapa_shared(smem_u32(act_full), 0);
     int g = 0, nin = 0;   // nin: steps whose input came through in_full (its phase)
     const uint64_t pol_last = policy_evict_last();
     // TMA stores of ACT boxes: with HC >= 64 each column group stores its own boxes
@@ -932,22 +949,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         if (wrote_act) fence_proxy_async_smem();
         __syncwarp();
         if (p.trace && blockIdx.x == 0 && g < 64 && lane == 0 && (w == 4 || w == 8)) p.trace[g * 8 + (w == 4 ? 5 : 6)] = clock64();
-#if XMGN_EPI_SINGLE_ARRIVE
-        // one release-arrive per CTA after the epilogue warps synchronise: only this
-        // warp's global stores sit in front of its release fence
-        named_bar(8, NEPI);
-        // hand-off timing in globaltimer ns (comparable across the pair): CTA 0 -> col 4, CTA 1 -> col 3
-        if (p.trace && blockIdx.x < 2 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 4 - (int)blockIdx.x] = gtimer();
-        if (threadIdx.x == 128) {
-          mbar_arrive_cluster(acc_empty_l);
-          if (wrote_act) mbar_arrive_cluster(act_full_l);
-        }
-#else
-        if (lane == 0) {
-          mbar_arrive_cluster(acc_empty_l);
-          if (wrote_act) mbar_arrive_cluster(act_full_l);
-        }
-#endif
+        // warp 3 arrives on the leader's barriers once every epilogue warp is here
+        named_bar(8, NEPI + 32);
       }
     }
   }
