@@ -368,7 +368,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
   const uint32_t rank = cluster_ctarank();
   const int cid = (int)cluster_id_x(), ncl = (int)n_clusters_x();
   const int n_tiles = (p.M + 255) / 256;     // pair tiles of 256 rows (128 per CTA)
-  constexpr int EPI_WARPS = NEPI / 32;
   constexpr int EPI_ARRIVALS = 1;   // warp 3, once per CTA and step
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::SA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
@@ -531,8 +530,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         named_bar(8, NEPI + 32);
         if (p.trace && blockIdx.x < 2 && g < 64 && lane_id() == 0) p.trace[g * 8 + 4 - (int)blockIdx.x] = gtimer();
         if (lane_id() == 0) {
-          mbar_arrive_cluster(acc_empty_l);
-          if (wa) mbar_arrive_cluster(act_full_l);
+          if (rank == 0) {          // the leader's own barriers: CTA-scope release suffices
+            mbar_arrive(acc_empty);
+            if (wa) mbar_arrive(act_full);
+          } else {
+            mbar_arrive_cluster(acc_empty_l);
+            if (wa) mbar_arrive_cluster(act_full_l);
+          }
         }
         __syncwarp();
       }
