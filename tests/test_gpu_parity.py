@@ -222,3 +222,22 @@ def test_single_partial_tile_many_partitions():
     res = run_gpu(b, 256, 3, FP16)
     ref = oracle_full(b, 256, 3)
     _check(res, ref, 256, 3, TAU[FP16])
+
+
+@pytest.mark.slow
+def test_cfg4_probe_gradients():
+    """CFG4 at the bench's full size and launch configuration (8 halo partitions,
+    H=512, L=15, FP16): with dL/dh^L non-zero on one probe row only, the parameter
+    gradient summed over the 8 partitions equals the probe's 15-hop-ball gradient,
+    which the FP64 oracle computes (partitioned = full graph)."""
+    b = configs.load("cfg4")
+    N = len(b["offsets"]) - 1
+    probe = int(np.random.default_rng(2).choice(N, 1)[0])
+    mask = np.zeros(N)
+    mask[probe] = 1.0
+    res = run_gpu(b, 512, 15, FP16, g_rows=mask, want_inputs=False)
+    o = oracle_probe(b, probe, 512, 15)
+    rms = np.sqrt((res["h"][b["owned"][:10000]] ** 2).mean())
+    assert np.abs(res["h"][probe] - o["h"]).max() <= TAU[FP16] * rms
+    gw, name = per_tensor_rel(res["params"], o["params"], 512, 15)
+    assert gw <= TAU[FP16], (gw, name)
