@@ -4,10 +4,10 @@
 
 namespace xmgn {
 
-template <int H, bool SPLIT, bool BWD, bool F16>
+template <int H, bool SPLIT, bool BWD, bool F16, bool Z1 = false>
 static void chain_launch(const ChainParams& p, int grid, cudaStream_t st) {
   using C = ChainCfg<H, SPLIT>;
-  auto kern = k_chain<H, SPLIT, BWD, F16>;
+  auto kern = k_chain<H, SPLIT, BWD, F16, Z1>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
@@ -24,7 +24,10 @@ size_t chain_smem(int H, bool split) {
 
 template <int H, bool F16>
 static void launch_h(bool bwd, const ChainParams& p, int grid, cudaStream_t st) {
-  if (bwd) chain_launch<H, false, true, F16>(p, grid, st);
+  bool z1 = false;
+  for (int i = 0; i < p.n_steps; ++i) z1 = z1 || (p.steps[i].flags & EF_FROM_IN) != 0;
+  if (bwd && z1) chain_launch<H, false, true, F16, true>(p, grid, st);
+  else if (bwd) chain_launch<H, false, true, F16>(p, grid, st);
   else chain_launch<H, false, false, F16>(p, grid, st);
 }
 

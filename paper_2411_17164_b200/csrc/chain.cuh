@@ -51,7 +51,9 @@ enum : int {
                          // (else only dgamma; the bias sums come from the wgrad GEMMs)
   EF_G16 = 512,        // EPI_LN_BWD / EPI_ADD: the gradient stream is the 16-bit g16 (edge programs):
                        // LN_BWD writes dY = g16 (+ ga16[dst]) back into g16; ADD does g16 += acc
-  EF_DISCARD = 2048    // EPI_DSILU: this is the last read of S' -- drop its L2 lines afterwards
+  EF_DISCARD = 2048,   // EPI_DSILU: this is the last read of S' -- drop its L2 lines afterwards
+  EF_STORE_Z = 8192,   // EPI_SILU (16-bit modes): round z to 16 bits, store it to scr_z, SiLU the rounded z
+  EF_FROM_IN = 16384   // EPI_SILU (16-bit modes): z is the TMA row input in ACT (a K = 0 step, no MMA)
 };
 
 enum : int {
@@ -334,7 +336,10 @@ __device__ __forceinline__ void load_dy(const Step& st, bool has_g, bool valid, 
 #include "epi16.cuh"
 namespace xmgn {
 
-template <int H, bool SPLIT, bool BWD, bool F16>
+// Z1: backward programs whose first edge step reloads the forward's z_1 checkpoint
+// (a separate instantiation so the regular backward kernel's register allocation is
+// unaffected)
+template <int H, bool SPLIT, bool BWD, bool F16, bool Z1 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THREADS, 1)
     k_chain(const __grid_constant__ ChainParams p) {
   using C = ChainCfg<H, SPLIT>;
@@ -906,7 +911,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
           constexpr int NC16 = HC / 16;
           const int op = st.epi;
           if (op == EPI_SILU) {
-            op_silu<H, NC16, F16>(e, st, wait);
+            if constexpr (Z1) {
+              if (st.flags & EF_FROM_IN) op_silu_in<H, NC16, F16>(e, st, wait);
+              else op_silu<H, NC16, F16, false>(e, st, wait);
+            } else {
+              op_silu<H, NC16, F16, !BWD>(e, st, wait);
+            }
             wrote_act = true;
           } else if (op == EPI_LN_FWD) {
             if (st.flags & EF_RES16) op_ln_fwd<H, NC16, F16, false>(e, st, wait, row_sum);

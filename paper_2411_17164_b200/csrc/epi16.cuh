@@ -220,7 +220,7 @@ __device__ __forceinline__ void ln_stats16(const Epi& e, float eps, RowSum row_s
 // loads that do not depend on it are issued first.
 
 // EPI_SILU: x = acc + b (+ P[src][c] + P[dst][H + c]) -> SiLU -> ACT (+ scratch A, S')
-template <int H, int NC, bool F16, class Wait>
+template <int H, int NC, bool F16, bool STZ, class Wait>
 __device__ __forceinline__ void op_silu(const Epi& e, const Step& st, Wait wait) {
   const bool gp = (st.flags & EF_GATHER_P) != 0;
   // A leaves by TMA from ACT when st_map is set, else by row stores
@@ -230,6 +230,8 @@ __device__ __forceinline__ void op_silu(const Epi& e, const Step& st, Wait wait)
   __nv_bfloat16* oa = st.scr_a + (size_t)e.r * H + e.cb;
   __nv_bfloat16* os = st.scr_s + (size_t)e.r * H + e.cb;
   const bool tsrc = gp && st.gsrc_map >= 0;   // P[src] rows arrive in ACT by TMA gather
+  const bool rz = STZ && (st.flags & EF_STORE_Z) != 0;   // keep z (16-bit) for the backward (fwd kernels)
+  __nv_bfloat16* oz = st.scr_z + (size_t)e.r * H + e.cb;
   uint32_t s0[8], d0[8], s1[8], d1[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) s0[i] = d0[i] = s1[i] = d1[i] = 0u;
@@ -263,6 +265,12 @@ __device__ __forceinline__ void op_silu(const Epi& e, const Step& st, Wait wait)
 #pragma unroll
     for (int i = 0; i < 16; ++i) x[i] += __uint_as_float(ta[i]);
     if (cc + 1 < NC) tmem_ld16_async(e.tl + (cc + 1) * 16, ta);
+    if constexpr (STZ) {
+      if (rz) {                         // the SiLU sees exactly the z the backward will reload
+        round16<F16>(x);
+        if (e.valid) st16<F16>(oz + cc * 16, x);
+      }
+    }
     if (ss) {
       float dv[16];
       silu_grad16<F16>(x, dv);
@@ -281,6 +289,35 @@ __device__ __forceinline__ void op_silu(const Epi& e, const Step& st, Wait wait)
   for (int cc = 0; cc < NC; cc += 2) {
     body(cc, s0, d0);
     body(cc + 1, s1, d1);
+  }
+}
+
+// EPI_SILU + EF_FROM_IN: a step without MMA whose z is the forward's 16-bit z_1
+// checkpoint, TMA-loaded into ACT (in_map): SiLU (+ SiLU') in place, A / S' out.
+// Compiled only into the Z1 variant of the backward kernel.
+template <int H, int NC, bool F16, class Wait>
+__device__ __forceinline__ void op_silu_in(const Epi& e, const Step& st, Wait wait) {
+  const bool sa = e.valid && (st.flags & EF_STORE_A) != 0 && st.st_map < 0, ss = (st.flags & EF_STORE_S) != 0;
+  __nv_bfloat16* oa = st.scr_a + (size_t)e.r * H + e.cb;
+  __nv_bfloat16* os = st.scr_s + (size_t)e.r * H + e.cb;
+  wait();
+#pragma unroll 1
+  for (int cc = 0; cc < NC; ++cc) {
+    float x[16];
+    in16<F16>(e, e.cb + cc * 16, x);
+    if (ss) {
+      float dv[16];
+      silu_grad16<F16>(x, dv);
+      if (e.valid) {
+        uint32_t h[8];
+        pack16x16<F16>(dv, h);
+        stg256_pol(os + cc * 16, h, e.pol_last);
+      }
+    } else {
+      silu16<F16>(x);
+    }
+    sts_tile16<F16>(e.act, e.trow, e.cb + cc * 16, x);
+    if (sa) st16<F16>(oa + cc * 16, x);
   }
 }
 

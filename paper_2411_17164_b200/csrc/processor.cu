@@ -52,6 +52,8 @@ struct xmgn_workspace {
   int njobs = 0;
   // checkpoints (per layer) and live streams
   xmgn::BfBuf e_ck, h_ck, a_ck;   // e_ck [L+1][Emax][H] (the 16-bit edge stream), h_ck / a_ck [L][Nmax][H]
+  xmgn::BfBuf z1_ck;              // [L][Emax][H] 16-bit z_1 of the edge MLP (16-bit modes, if HBM allows)
+  bool use_z1 = false;
   float *h_buf[2] = {nullptr, nullptr};
   xmgn::BfBuf P;                  // node pre-projections, one per layer [L][Nmax][2H], 16-bit (kept for the bwd)
   // backward
@@ -422,6 +424,19 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
       ws->part = (float*)dalloc(ws, (size_t)ws->part_splits * (2 * H + 128) * H * 4);
       ws->colsum = (float*)dalloc(ws, (size_t)ws->sms * 4 * NV_MAX * H * 4);
       ws->d_flag = (int*)dalloc(ws, 4);
+      // Opt-in (XMGN_Z1=1) memory-for-speed mode: z_1 checkpoints (+L x E x H x 2 bytes) let
+      // the backward skip the first edge GEMM's recompute (edge bwd -5%).  Off by default: at
+      // CFG4 on one GPU they would not leave room for the 62 GB of resident inputs.
+      const char* z1env = getenv("XMGN_Z1");
+      if (!ws->split && z1env && atoi(z1env) == 1) {
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        const size_t need = (size_t)L * EH * sizeof(bf16);
+        if (free_b > need + ((size_t)8 << 30)) {
+          ws->z1_ck = bfalloc(ws, (size_t)L * EH);
+          ws->use_z1 = true;
+        }
+      }
     } catch (...) {
       xmgn_workspace_free(ws);
       throw;
@@ -497,6 +512,7 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
           if (j == 0) {
             s.flags |= EF_GATHER_P; s.gather16 = Pl(li); s.gather16_lo = ws->P.lo;
             if (!ws->split) s.gsrc_map = pr.gather_map(Pl(li), P.n_local, 2 * H);
+            if (ws->use_z1) { s.flags |= EF_STORE_Z; s.scr_z = ws->z1_ck.p + (long long)li * EH; }
           }
         }
         // e^l = e^{l-1} + LN(..): the edge stream itself is 16-bit (checkpoint = next operand)
@@ -597,8 +613,15 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
           s.scr_a = ws->scrA[j].p; s.scr_s = ws->scrS[j].p; s.lo_off = ws->scrA[j].lo;
           if (!ws->split && rows > 0) s.st_map = pr.in_map(ws->scrA[j].p, rows, H);   // A_j = the ACT tile, TMA-stored
           if (j == 0 && blk == 0) {
-            s.flags |= EF_GATHER_P; s.gather16 = Pl(li); s.gather16_lo = ws->P.lo;
-            if (!ws->split) s.gsrc_map = pr.gather_map(Pl(li), P.n_local, 2 * H);
+            if (ws->use_z1 && rows > 0) {
+              // z_1 from the forward's checkpoint: no GEMM, no gathers (a K = 0 step)
+              s.K = 0; s.bias = nullptr;
+              s.flags |= EF_FROM_IN;
+              s.in_map = pr.in_map(ws->z1_ck.p + (long long)li * EH, rows, H);
+            } else {
+              s.flags |= EF_GATHER_P; s.gather16 = Pl(li); s.gather16_lo = ws->P.lo;
+              if (!ws->split) s.gsrc_map = pr.gather_map(Pl(li), P.n_local, 2 * H);
+            }
           }
         }
         Step& s = pr.add();

@@ -241,3 +241,13 @@ def test_cfg4_probe_gradients():
     assert np.abs(res["h"][probe] - o["h"]).max() <= TAU[FP16] * rms
     gw, name = per_tensor_rel(res["params"], o["params"], 512, 15)
     assert gw <= TAU[FP16], (gw, name)
+
+
+def test_z1_checkpoint_mode(monkeypatch):
+    """Opt-in XMGN_Z1=1: the forward keeps z_1 and the backward replaces the first edge
+    GEMM's recompute by a K = 0 step that reloads it; same parity bound as the default."""
+    monkeypatch.setenv("XMGN_Z1", "1")
+    b = configs.custom((300, 1500), k=6, P=4, halo=3)
+    res = run_gpu(b, 512, 3, FP16)
+    ref = oracle_full(b, 512, 3)
+    _check(res, ref, 512, 3, TAU[FP16])
