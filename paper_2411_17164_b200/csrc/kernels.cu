@@ -79,7 +79,28 @@ __global__ void __launch_bounds__(256) k_aggregate(const int* __restrict__ off, 
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int k0 = off[i], k1 = off[i + 1];
-    for (int k = k0; k < k1; ++k) {
+    int k = k0;
+    if (!e_lo) {
+      // batches of B edges: all B x V row loads in flight before any is summed (memory-level
+      // parallelism); the sums still run in CSR order
+      constexpr int B = 4;
+      for (; k + B <= k1; k += B) {
+        uint2 u[B][V];
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+#pragma unroll
+          for (int v = 0; v < V; ++v) u[b][v] = __ldg(reinterpret_cast<const uint2*>(e + (size_t)(k + b) * H) + lane + 32 * v);
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            float x[4];
+            unpack4<F16>(u[b][v], x);
+            acc[v].x += x[0]; acc[v].y += x[1]; acc[v].z += x[2]; acc[v].w += x[3];
+          }
+      }
+    }
+    for (; k < k1; ++k) {
       const uint2* row = reinterpret_cast<const uint2*>(e + (size_t)k * H);
 #pragma unroll
       for (int v = 0; v < V; ++v) {
