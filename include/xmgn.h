@@ -119,9 +119,14 @@ typedef struct {
 } xmgn_model_cfg;
 
 size_t xmgn_param_count(const xmgn_model_cfg* cfg);
-/* Workspace for one GPU: per-layer BF16 checkpoints, scratch and gradient
- * streams sized for the graph's largest partition; reused across that GPU's
- * sequential partitions.  Requires cfg->layers <= halo depth (else EHALO).    */
+/* Workspace for one GPU: per-layer 16-bit checkpoints (edge stream, node
+ * states, aggregates, node pre-projections), scratch and gradient streams sized
+ * for the graph's largest partition; reused across that GPU's sequential
+ * partitions.  Requires cfg->layers <= halo depth (else EHALO).  With the
+ * environment variable XMGN_Z1=1 (16-bit modes) it also keeps the first edge
+ * GEMM's pre-activation per layer (+layers x E_max x H x 2 bytes), which lets
+ * xmgn_processor_bwd skip that GEMM's recompute; results stay within the same
+ * tolerance.  xmgn_workspace_bytes reports the total allocated.              */
 xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_model_cfg* cfg, xmgn_workspace** out);
 size_t xmgn_workspace_bytes(const xmgn_workspace* ws);
 void xmgn_workspace_free(xmgn_workspace* ws);
