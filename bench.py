@@ -154,6 +154,18 @@ def scope_work(info, H_=H, L_=L, m=M_HID):
     return w, agg_bytes, rows
 
 
+def relaunch(n):
+    """`bench.py --gpus N` outside torchrun: start N ranks (one process per GPU,
+    NCCL) on this node with torch.distributed.run and pass rank 0's output through."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -165,6 +177,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "xmgn":
+        return relaunch(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -413,4 +427,4 @@ def reference(args, world, rank):
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

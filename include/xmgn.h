@@ -126,7 +126,9 @@ size_t xmgn_param_count(const xmgn_model_cfg* cfg);
  * environment variable XMGN_Z1=1 (16-bit modes) it also keeps the first edge
  * GEMM's pre-activation per layer (+layers x E_max x H x 2 bytes), which lets
  * xmgn_processor_bwd skip that GEMM's recompute; results stay within the same
- * tolerance.  xmgn_workspace_bytes reports the total allocated.              */
+ * tolerance.  If that extra allocation fails the call returns ENOMEM (no silent
+ * fall-back); XMGN_Z1=1 with the FP32 check mode is EUNSUPPORTED.
+ * xmgn_workspace_bytes reports the total allocated.                          */
 xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_model_cfg* cfg, xmgn_workspace** out);
 size_t xmgn_workspace_bytes(const xmgn_workspace* ws);
 void xmgn_workspace_free(xmgn_workspace* ws);

@@ -1,5 +1,6 @@
 // Instantiations and launcher of the GEMM-chain kernel (chain.cuh).
 #include <cuda_runtime.h>
+#include <atomic>
 #include "kernels_launch.h"
 
 namespace xmgn {
@@ -8,10 +9,14 @@ template <int H, bool SPLIT, bool BWD, bool F16, bool Z1 = false>
 static void chain_launch(const ChainParams& p, int grid, cudaStream_t st) {
   using C = ChainCfg<H, SPLIT>;
   auto kern = k_chain<H, SPLIT, BWD, F16, Z1>;
-  static bool attr = false;
-  if (!attr) {
+  // the smem attribute is per device context: one flag per device (set idempotently,
+  // so two host threads racing on the same device are harmless)
+  static std::atomic<bool> attr[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr[dev].load(std::memory_order_acquire)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-    attr = true;
+    if (dev >= 0 && dev < 64) attr[dev].store(true, std::memory_order_release);
   }
   kern<<<grid, EpiShape<SPLIT>::THREADS, C::SMEM_BYTES, st>>>(p);
 }

@@ -134,8 +134,6 @@ struct ChainParams {
   const int* dst;     // [M] destination local id
   float* colsum;      // [gridDim.x][4][NV_MAX][H] partial column sums (backward)
   float eps;          // LayerNorm epsilon
-  unsigned long long* trace;  // debug: per-step clock64 stamps of CTA 0 (nullptr = off)
-  int dbg;                    // debug experiment bits (0 in production)
 };
 
 template <int H, bool SPLIT>
@@ -163,11 +161,6 @@ struct ChainCfg {
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 __device__ __forceinline__ float sigmoid_fast(float v) {
   float t;
   asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * v));
@@ -393,13 +386,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  if (p.dbg > 0) {
-    // experiment: stagger the start of clusters by (cid % 4) * dbg microseconds so the
-    // pairs' memory-heavy epilogue phases do not all coincide
-    const unsigned long long t0 = clock64();
-    const unsigned long long wait_cyc = (unsigned long long)(cid % 4) * (unsigned long long)p.dbg * 1900ull;
-    while (clock64() - t0 < wait_cyc) __nanosleep(1000);
-  }
 
   // register split (setmaxnreg, per warpgroup): control warps 0-3 need few registers,
   // the epilogue warpgroups get the rest
@@ -457,7 +443,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
           // the previous epilogue must be done (it may still read its input out of ACT)
           // before ACT can become A-ring space again
           if (g > 0) mbar_wait(acc_empty, (g - 1) & 1);
-          if (p.trace && blockIdx.x == 0 && g < 64 && lane_id() == 0) p.trace[g * 8 + 7] = gtimer();
           if (tma_a && g > 0 && (st.ctl & CTL_NEED_ACT_FREE)) {
             // let every issued MMA (the ones reading ACT) retire, then hand both
             // CTAs' ACT tiles to their producers as A-ring space.
@@ -470,7 +455,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
           }
           if (st.ctl & CTL_WAIT_ACT) { mbar_wait(act_full, nact & 1); ++nact; }
           tc_fence_after();
-          if (p.trace && blockIdx.x == 0 && g < 64 && lane_id() == 0) p.trace[g * 8 + 0] = clock64();
           for (int kc = 0; kc < st.K / 64; ++kc) {
             int aslot = 0;
             uint32_t a_base;
@@ -515,7 +499,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
           }
           if (elect_one()) mma_commit_cg2_mc(acc_full, 3);
           __syncwarp();
-          if (p.trace && blockIdx.x == 0 && g < 64 && lane_id() == 0) p.trace[g * 8 + 1] = clock64();
         }
       }
     }
@@ -533,7 +516,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         const bool wa = st.epi == EPI_SILU || st.epi == EPI_LN_BWD || st.epi == EPI_DSILU ||
                         (st.epi == EPI_LN_FWD && (st.flags & EF_WRITE_ACT));
         named_bar(8, NEPI + 32);
-        if (p.trace && blockIdx.x < 2 && g < 64 && lane_id() == 0) p.trace[g * 8 + 4 - (int)blockIdx.x] = gtimer();
         if (lane_id() == 0) {
           if (rank == 0) {          // the leader's own barriers: CTA-scope release suffices
             mbar_arrive(acc_empty);
@@ -602,7 +584,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         if constexpr (SPLIT) {
         mbar_wait(acc_full, g & 1);
         tc_fence_after();
-        if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 2] = clock64();
         float v[32], pb[32];
         if (st.epi == EPI_SILU && !(st.flags & (EF_GATHER_P | EF_STORE_S | EF_STORE_A))) {
           // plain SiLU epilogue, software-pipelined one chunk ahead (TMEM + bias)
@@ -660,19 +641,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
           wrote_act = true;
         } else if (st.epi == EPI_LN_FWD || st.epi == EPI_LN_BWD) {
           // z = acc + b; mean and variance over the H columns of this row in one TMEM pass
-          // (sum and sum of squares in FP32; var = E[z^2] - mean^2, clamped at 0)
-          float sum = 0.f, sq = 0.f;
+          // (shifted partial moments per thread + exact group combination, as ln_stats16)
+          float sum = 0.f, sq = 0.f, kz = 0.f;
 #pragma unroll 1
           for (int cc = 0; cc < NC; ++cc) {
             tmem_ld32(tl + cc * 32, v);
             load_f32x32_ro(st.bias + cb + cc * 32, pb);
+            if (cc == 0) kz = v[0] + pb[0];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) { const float z = v[i] + pb[i]; sum += z; sq = fmaf(z, z, sq); }
+            for (int i = 0; i < 32; ++i) { const float z = v[i] + pb[i] - kz; sum += z; sq = fmaf(z, z, sq); }
           }
-          const float mean = row_sum(sum) * (1.0f / H);
-          const float var = fmaxf(row_sum(sq) * (1.0f / H) - mean * mean, 0.f);
+          const float mg = kz + sum * (1.0f / HC);
+          const float m2 = fmaxf(sq - sum * sum * (1.0f / HC), 0.f);
+          const float mean = row_sum(mg) * (1.0f / EW);
+          const float dmg = mg - mean;
+          const float var = row_sum(fmaf((float)HC * dmg, dmg, m2)) * (1.0f / H);
           const float rstd = rsqrtf(var + p.eps);
-          if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 3] = clock64();
           if (st.epi == EPI_LN_FWD) {
 #pragma unroll 1
             for (int cc = 0; cc < NC; ++cc) {
@@ -745,8 +729,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
             }
             s1 = row_sum(s1) * (1.0f / H);
             s2 = row_sum(s2) * (1.0f / H);
-            // hand-off timing in globaltimer ns (comparable across the pair): CTA 0 -> col 4, CTA 1 -> col 3
-        if (p.trace && blockIdx.x < 2 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 4 - (int)blockIdx.x] = gtimer();
 #pragma unroll 1
             for (int cc = 0; cc < NC; ++cc) {
               const int c0 = cb + cc * 32;
@@ -866,7 +848,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
             named_bar(7, NEPI);
             mbar_wait(acc_full, g & 1);
             tc_fence_after();
-            if (p.trace && blockIdx.x == 0 && g < 64 && threadIdx.x == 128) p.trace[g * 8 + 2] = clock64();
             if (st_pending) {   // the previous step's stores must have read ACT before anything rewrites it
               if (issuer) bulk_wait_read0();
               named_bar(13, NEPI);
@@ -937,6 +918,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
               wrote_act = true;
             }
           }
+          // rows this step wrote with ordinary stores that a later step of this kernel reads
+          // back by TMA (S' -> the dSiLU steps, G_e' -> the dX step): order the generic-proxy
+          // writes before those async-proxy reads (the end-of-step barrier carries the order
+          // to the TMA-issuing thread)
+          if ((op == EPI_SILU && (st.flags & EF_STORE_S)) || (op == EPI_LN_BWD && (st.flags & EF_G16)))
+            fence_proxy_async_global();
           if (st.in_map >= 0 || st.gsrc_map >= 0) ++nin;
           if (st.st_map >= 0) {
             // this thread-set's ACT boxes -> global rows [row0, row0 + 128) by TMA
@@ -962,7 +949,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         tc_fence_before();
         if (wrote_act) fence_proxy_async_smem();
         __syncwarp();
-        if (p.trace && blockIdx.x == 0 && g < 64 && lane == 0 && (w == 4 || w == 8)) p.trace[g * 8 + (w == 4 ? 5 : 6)] = clock64();
         // warp 3 arrives on the leader's barriers once every epilogue warp is here
         named_bar(8, NEPI + 32);
       }

@@ -83,6 +83,8 @@ extern "C" xmgn_status xmgn_comm_init(const uint8_t id[128], int nranks, int ran
 extern "C" xmgn_status xmgn_grad_reduce(xmgn_comm* c, float* grad, size_t count, void* stream) {
   if (!c || (!grad && count)) return set_error(XMGN_EINVAL, "xmgn_grad_reduce: null argument");
   XMGN_NEED_NCCL("xmgn_grad_reduce");
+  cudaError_t e = cudaSetDevice(c->device);   // the communicator's device must be current
+  if (e != cudaSuccess) return cuda_status(e, "xmgn_grad_reduce: cudaSetDevice");
   return nccl_status(nccl().allReduce(grad, grad, count, ncclFloat32, ncclSum, c->comm, (cudaStream_t)stream),
                      "xmgn_grad_reduce");
 }

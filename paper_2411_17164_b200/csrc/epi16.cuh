@@ -187,13 +187,18 @@ __device__ __forceinline__ void colsum16_add(const Epi& e, int vec, int c0, floa
   }
 }
 
-// Row statistics (mean, rstd) of z = acc + b over the H columns of this row
-// (one TMEM pass; var = E[z^2] - mean^2 clamped at 0).  row_sum combines the
-// EW column groups in a fixed order.
+// Row statistics (mean, rstd) of z = acc + b over the H columns of this row, in
+// one TMEM pass without the cancellation of E[z^2] - mean^2: each thread sums its
+// HC columns shifted by its own first value k (S1 = sum(z - k), S2 = sum(z - k)^2,
+// so its partial M2 = S2 - S1^2 / HC loses nothing when |mean| >> sigma), and the
+// EW column groups are combined exactly (Chan et al.): mean = avg of the group
+// means, M2 = sum_g (M2_g + HC (mean_g - mean)^2); var = M2 / H (biased).
+// row_sum combines the groups in a fixed order.
 template <int H, int NC, class RowSum>
 __device__ __forceinline__ void ln_stats16(const Epi& e, float eps, RowSum row_sum, float& mean, float& rstd) {
-  constexpr int HTOT = H;
-  float sum = 0.f, sq = 0.f;
+  constexpr int HC = NC * 16;          // columns of this thread
+  constexpr int EW = H / HC;           // column groups per row
+  float s1 = 0.f, s2 = 0.f, k = 0.f;
   uint32_t ta[16];
   tmem_ld16_async(e.tl, ta);
 #pragma unroll 1
@@ -204,14 +209,19 @@ __device__ __forceinline__ void ln_stats16(const Epi& e, float eps, RowSum row_s
 #pragma unroll
     for (int i = 0; i < 16; ++i) b[i] += __uint_as_float(ta[i]);
     if (cc + 1 < NC) tmem_ld16_async(e.tl + (cc + 1) * 16, ta);
+    if (cc == 0) k = b[0];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      sum += b[i];
-      sq = fmaf(b[i], b[i], sq);
+      const float d = b[i] - k;
+      s1 += d;
+      s2 = fmaf(d, d, s2);
     }
   }
-  mean = row_sum(sum) * (1.0f / HTOT);
-  const float var = fmaxf(row_sum(sq) * (1.0f / HTOT) - mean * mean, 0.f);
+  const float mg = k + s1 * (1.0f / HC);
+  const float m2 = fmaxf(s2 - s1 * s1 * (1.0f / HC), 0.f);
+  mean = row_sum(mg) * (1.0f / EW);
+  const float dm = mg - mean;
+  const float var = row_sum(fmaf((float)HC * dm, dm, m2)) * (1.0f / H);
   rstd = rsqrtf(var + eps);
 }
 

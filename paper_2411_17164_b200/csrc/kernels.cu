@@ -49,7 +49,8 @@ __global__ void k_to_bf16(const float* __restrict__ in, __nv_bfloat16* __restric
 // ---------------------------------------------------------------- 16-bit (hi [+ lo]) -> FP32
 template <bool F16>
 __global__ void k_to_f32(const __nv_bfloat16* __restrict__ in, long long lo_off, float* __restrict__ out,
-                         long long n8) {
+                         long long n8, const float* __restrict__ inv) {
+  const float u = inv ? *inv : 1.0f;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n8; t += (long long)gridDim.x * blockDim.x) {
     float v[8];
     unpack8<F16>(reinterpret_cast<const uint4*>(in)[t], v);
@@ -59,6 +60,8 @@ __global__ void k_to_f32(const __nv_bfloat16* __restrict__ in, long long lo_off,
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] += w[i];
     }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] *= u;
     reinterpret_cast<float4*>(out)[2 * t] = make_float4(v[0], v[1], v[2], v[3]);
     reinterpret_cast<float4*>(out)[2 * t + 1] = make_float4(v[4], v[5], v[6], v[7]);
   }
@@ -126,6 +129,50 @@ __global__ void __launch_bounds__(256) k_aggregate(const int* __restrict__ off, 
         split2<F16, false>(acc[v].x, acc[v].y, h0, l0);
         split2<F16, false>(acc[v].z, acc[v].w, h1, l1);
       }
+      reinterpret_cast<uint2*>(a + (size_t)i * H)[lane + 32 * v] = make_uint2(h0, h1);
+    }
+  }
+}
+
+// Aggregation from an FP32 edge stream (BF16 mode keeps the edge residual stream in
+// FP32, SURVEY §7.3 H1 rung R1): same order and output as k_aggregate.
+template <int H, bool F16>
+__global__ void __launch_bounds__(256) k_aggregate32(const int* __restrict__ off, const float* __restrict__ e,
+                                                     __nv_bfloat16* __restrict__ a, int n) {
+  constexpr int V = H / 4 / 32;  // float4 groups per lane
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
+    float4 acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int k0 = off[i], k1 = off[i + 1];
+    int k = k0;
+    constexpr int B = 4;
+    for (; k + B <= k1; k += B) {
+      float4 u[B][V];
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+#pragma unroll
+        for (int v = 0; v < V; ++v) u[b][v] = __ldg(reinterpret_cast<const float4*>(e + (size_t)(k + b) * H) + lane + 32 * v);
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          acc[v].x += u[b][v].x; acc[v].y += u[b][v].y; acc[v].z += u[b][v].z; acc[v].w += u[b][v].w;
+        }
+    }
+    for (; k < k1; ++k) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(e + (size_t)k * H) + lane + 32 * v);
+        acc[v].x += x.x; acc[v].y += x.y; acc[v].z += x.z; acc[v].w += x.w;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      uint32_t h0, h1, l0, l1;
+      split2<F16, false>(acc[v].x, acc[v].y, h0, l0);
+      split2<F16, false>(acc[v].z, acc[v].w, h1, l1);
       reinterpret_cast<uint2*>(a + (size_t)i * H)[lane + 32 * v] = make_uint2(h0, h1);
     }
   }
@@ -337,26 +384,64 @@ __global__ void __launch_bounds__(128, 1) k_wgrad(const __grid_constant__ WgradP
   if (w == 2) tmem_dealloc(tmem, NT);
 }
 
-// grad[i] += sum_{s < S} part[s][i] for i < n, split stride `ld` (fixed order)
+// grad[i] += unscale * sum_{s < S} part[s][i] for i < n, split stride `ld` (fixed order);
+// unscale = inv[0] (the backward's power-of-two loss-scale inverse, exact) or 1
 __global__ void k_reduce_part(const float* __restrict__ part, int S, long long n, long long ld,
-                              float* __restrict__ grad) {
+                              float* __restrict__ grad, const float* __restrict__ inv) {
+  const float u = inv ? *inv : 1.0f;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int k = 0; k < S; ++k) s += part[k * ld + i];
-    grad[i] += s;
+    grad[i] += s * u;
   }
 }
 
 // Column-sum partials [nblk][4][NV][H] -> grad[dst[v] + c] += sum (fixed order).
 __global__ void k_reduce_colsum(const float* __restrict__ part, int nblk, int nv, int H, ColsumDst dsts,
-                                float* __restrict__ grad) {
+                                float* __restrict__ grad, const float* __restrict__ inv) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nv * H) return;
   const int v = t / H, c = t % H;
   if (dsts.off[v] < 0) return;
   float s = 0.f;
   for (int b = 0; b < nblk * 4; ++b) s += part[((size_t)b * NV_COLSUM + v) * H + c];
-  grad[dsts.off[v] + c] += s;
+  grad[dsts.off[v] + c] += s * (inv ? *inv : 1.0f);
+}
+
+// ---------------------------------------------------------------- loss scaling of the backward
+// The backward is linear in the upstream gradient g.  Its 16-bit gradient streams
+// (G_e, G_a, dZ, D) would flush an MSE-normalised g (|g| ~ 1e-7) to
+// FP16 zero, so the seed is scaled by a power of two S that puts max|g| in [1, 2),
+// and every gradient leaving the library is multiplied by 1/S.  Both are exact in
+// binary floating point, so results equal the unscaled arithmetic (bitwise when
+// S = 1, i.e. max|g| already in [1, 2)).
+__global__ void k_amax(const float* __restrict__ x, long long n, unsigned int* __restrict__ amax_bits) {
+  unsigned int m = 0u;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(x[i]) & 0x7fffffffu);   // |x| bits: integer order = float order (NaN above inf)
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(amax_bits, m);   // max is order-independent: deterministic
+}
+// scale[0] = S, scale[1] = 1/S; out = S * g
+__global__ void k_seed_scale(const float* __restrict__ g, long long n, const unsigned int* __restrict__ amax_bits,
+                             float* __restrict__ out, float* __restrict__ scale) {
+  const unsigned int a = *amax_bits;
+  const int ex = (int)((a >> 23) & 0xffu);
+  // normal finite amax = 1.f * 2^(ex - 127): S = 2^(127 - ex); zero, subnormal or non-finite: S = 1
+  const int sh = (ex == 0 || ex == 255) ? 0 : 127 - ex;
+  const int shc = sh > 100 ? 100 : (sh < -100 ? -100 : sh);
+  const float S = ldexpf(1.0f, shc), inv = ldexpf(1.0f, -shc);
+  if (blockIdx.x == 0 && threadIdx.x == 0) { scale[0] = S; scale[1] = inv; }
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = g[i] * S;
+}
+// out = in * inv[0]
+__global__ void k_scale_copy(const float* __restrict__ in, long long n, const float* __restrict__ inv,
+                             float* __restrict__ out) {
+  const float u = *inv;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = in[i] * u;
 }
 
 __global__ void k_nonfinite(const float* __restrict__ x, long long n, int* __restrict__ flag) {
@@ -380,13 +465,27 @@ void launch_to_bf16(bool f16, const float* in, __nv_bfloat16* out, long long lo_
   if (f16) k_to_bf16<true><<<blocks, 256, 0, st>>>(in, out, lo_off, n8);
   else k_to_bf16<false><<<blocks, 256, 0, st>>>(in, out, lo_off, n8);
 }
-void launch_to_f32(bool f16, const __nv_bfloat16* in, long long lo_off, float* out, long long n, cudaStream_t st) {
+void launch_to_f32(bool f16, const __nv_bfloat16* in, long long lo_off, float* out, long long n, cudaStream_t st,
+                   const float* inv) {
   if (n <= 0) return;
   count_launch();
   long long n8 = n / 8;
   int blocks = (int)std::min<long long>((n8 + 255) / 256, 148 * 16);
-  if (f16 && !lo_off) k_to_f32<true><<<blocks, 256, 0, st>>>(in, lo_off, out, n8);
-  else k_to_f32<false><<<blocks, 256, 0, st>>>(in, lo_off, out, n8);
+  if (f16 && !lo_off) k_to_f32<true><<<blocks, 256, 0, st>>>(in, lo_off, out, n8, inv);
+  else k_to_f32<false><<<blocks, 256, 0, st>>>(in, lo_off, out, n8, inv);
+}
+void launch_seed_scale(const float* g, long long n, unsigned int* amax_bits, float* out, float* scale, cudaStream_t st) {
+  cudaMemsetAsync(amax_bits, 0, sizeof(unsigned int), st);
+  count_launch(2);
+  const int blocks = (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 4));
+  k_amax<<<blocks, 256, 0, st>>>(g, n, amax_bits);
+  k_seed_scale<<<blocks, 256, 0, st>>>(g, n, amax_bits, out, scale);
+}
+void launch_scale_copy(const float* in, long long n, const float* inv, float* out, cudaStream_t st) {
+  if (n <= 0) return;
+  count_launch();
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+  k_scale_copy<<<blocks, 256, 0, st>>>(in, n, inv, out);
 }
 
 template <bool F16>
@@ -402,6 +501,14 @@ void launch_aggregate(bool f16, int H, const int* off, const __nv_bfloat16* e, l
   if (n <= 0) return;
   count_launch();
   if (f16) agg_t<true>(H, off, e, e_lo, a, lo_off, n, st); else agg_t<false>(H, off, e, e_lo, a, lo_off, n, st);
+}
+void launch_aggregate32(int H, const int* off, const float* e, __nv_bfloat16* a, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  count_launch();
+  int blocks = std::min((n + 7) / 8, 148 * 16);
+  if (H == 128) k_aggregate32<128, false><<<blocks, 256, 0, st>>>(off, e, a, n);
+  else if (H == 256) k_aggregate32<256, false><<<blocks, 256, 0, st>>>(off, e, a, n);
+  else k_aggregate32<512, false><<<blocks, 256, 0, st>>>(off, e, a, n);
 }
 template <bool F16>
 static void seg_t(int H, const int* off, const int* rev, const __nv_bfloat16* dz, long long dz_lo, __nv_bfloat16* D,
@@ -441,14 +548,16 @@ void launch_wgrad(const WgradParams& p, bool split, bool f16, cudaStream_t st) {
     else wgrad_launch<128, false, false>(p, grid, st);
   }
 }
-void launch_reduce_part(const float* part, int S, long long n, long long ld, float* grad, cudaStream_t st) {
+void launch_reduce_part(const float* part, int S, long long n, long long ld, float* grad, cudaStream_t st,
+                        const float* inv) {
   count_launch();
   int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
-  k_reduce_part<<<blocks, 256, 0, st>>>(part, S, n, ld, grad);
+  k_reduce_part<<<blocks, 256, 0, st>>>(part, S, n, ld, grad, inv);
 }
-void launch_reduce_colsum(const float* part, int nblk, int nv, int H, ColsumDst d, float* grad, cudaStream_t st) {
+void launch_reduce_colsum(const float* part, int nblk, int nv, int H, ColsumDst d, float* grad, cudaStream_t st,
+                          const float* inv) {
   count_launch();
-  k_reduce_colsum<<<(nv * H + 255) / 256, 256, 0, st>>>(part, nblk, nv, H, d, grad);
+  k_reduce_colsum<<<(nv * H + 255) / 256, 256, 0, st>>>(part, nblk, nv, H, d, grad, inv);
 }
 void launch_nonfinite(const float* x, long long n, int* flag, cudaStream_t st) {
   count_launch();

@@ -15,15 +15,23 @@ struct ColsumDst {
 
 // `f16`: the 16-bit operand buffers hold FP16 instead of BF16 (XMGN_PREC_FP16).
 void launch_pack(bool f16, const float* params, const PackJob* jobs, int njobs, cudaStream_t st);
-void launch_to_f32(bool f16, const __nv_bfloat16* in, long long lo_off, float* out, long long n, cudaStream_t st);
+void launch_to_f32(bool f16, const __nv_bfloat16* in, long long lo_off, float* out, long long n, cudaStream_t st,
+                   const float* inv = nullptr);
+// backward loss scaling: scale = {S, 1/S} with S = 2^k putting max|g| in [1, 2); out = S g
+void launch_seed_scale(const float* g, long long n, unsigned int* amax_bits, float* out, float* scale, cudaStream_t st);
+void launch_scale_copy(const float* in, long long n, const float* inv, float* out, cudaStream_t st);
 void launch_to_bf16(bool f16, const float* in, __nv_bfloat16* out, long long lo_off, long long n, cudaStream_t st);
 void launch_aggregate(bool f16, int H, const int* off, const __nv_bfloat16* e, long long e_lo, __nv_bfloat16* a,
                       long long lo_off, int n, cudaStream_t st);
+// BF16 mode: a (BF16) = CSR-order FP32 sums of the FP32 edge stream
+void launch_aggregate32(int H, const int* off, const float* e, __nv_bfloat16* a, int n, cudaStream_t st);
 void launch_segsum(bool f16, int H, const int* off, const int* rev, const __nv_bfloat16* dz, long long dz_lo,
                    __nv_bfloat16* D, long long d_lo, int n, int e_act, cudaStream_t st);
 void launch_wgrad(const WgradParams& p, bool split, bool f16, cudaStream_t st);
-void launch_reduce_part(const float* part, int S, long long n, long long ld, float* grad, cudaStream_t st);
-void launch_reduce_colsum(const float* part, int nblk, int nv, int H, ColsumDst d, float* grad, cudaStream_t st);
+void launch_reduce_part(const float* part, int S, long long n, long long ld, float* grad, cudaStream_t st,
+                        const float* inv = nullptr);
+void launch_reduce_colsum(const float* part, int nblk, int nv, int H, ColsumDst d, float* grad, cudaStream_t st,
+                          const float* inv = nullptr);
 void launch_nonfinite(const float* x, long long n, int* flag, cudaStream_t st);
 // profiling (processor.cu): every kernel launch of the library is counted;
 // when enabled, named launch scopes are bracketed by CUDA events on their stream.

@@ -55,6 +55,8 @@ struct xmgn_workspace {
   xmgn::BfBuf z1_ck;              // [L][Emax][H] 16-bit z_1 of the edge MLP (16-bit modes, if HBM allows)
   bool use_z1 = false;
   float *h_buf[2] = {nullptr, nullptr};
+  float *e32[2] = {nullptr, nullptr};  // BF16 mode: the edge residual stream in FP32 (ping-pong)
+  bool e32_mode = false;
   xmgn::BfBuf P;                  // node pre-projections, one per layer [L][Nmax][2H], 16-bit (kept for the bwd)
   // backward
   float* Gh = nullptr;            // dL/dh (FP32, node level)
@@ -63,7 +65,8 @@ struct xmgn_workspace {
   float* part = nullptr;  // wgrad split-K partials
   int part_splits = 0;
   float* colsum = nullptr;
-  int* d_flag = nullptr;
+  unsigned int* d_amax = nullptr;  // max|g| bits of the current backward's seed
+  float* d_scale = nullptr;        // {S, 1/S}: the backward's power-of-two loss scale
   int last_fwd = -1;
 };
 
@@ -150,8 +153,8 @@ static std::vector<PackJob> pack_jobs(xmgn_workspace* ws) {
 }
 
 // ---- tensor maps
-static CUtensorMap map_rows(const bf16* base, long long rows, int width, int box_rows) {
-  return tmap_bf16(base, (uint64_t)width, (uint64_t)(rows > 0 ? rows : 1), (uint64_t)width, 64, box_rows);
+static CUtensorMap map_rows(const bf16* base, long long rows, int width, int box_rows, bool f16) {
+  return tmap16(base, (uint64_t)width, (uint64_t)(rows > 0 ? rows : 1), (uint64_t)width, 64, box_rows, f16);
 }
 
 // ---- chain program builder
@@ -159,7 +162,8 @@ struct Prog {
   ChainParams p;
   int n = 0;
   int next_map = 8;   // map slots 8.. hold the epilogues' TMA row inputs
-  Prog() { std::memset(&p, 0, sizeof(p)); }
+  bool f16 = false;   // tensor-map element type of the 16-bit operands
+  explicit Prog(const xmgn_workspace* ws) : f16(ws->f16) { std::memset(&p, 0, sizeof(p)); }
   Step& add() {
     Step& s = p.steps[n++];
     std::memset(&s, 0, sizeof(s));
@@ -172,14 +176,14 @@ struct Prog {
   // TMA gather source over P [rows][2H] 16-bit: 1-row boxes of 64 columns
   int gather_map(const bf16* base, long long rows, int width) {
     if (next_map >= MAX_MAPS) throw Fail{set_error(XMGN_ESTATE, "internal: out of tensor-map slots")};
-    p.maps[next_map] = tmap_bf16(base, width, (uint64_t)(rows > 0 ? rows : 1), width, 64, 1);
+    p.maps[next_map] = tmap16(base, width, (uint64_t)(rows > 0 ? rows : 1), width, 64, 1, f16);
     return next_map++;
   }
   // TMA source of an epilogue row input: 16-bit rows [0, rows) x H, rows > 0 (rows beyond read zero)
   int in_map(const bf16* base, long long rows, int H) {
     if (next_map >= MAX_MAPS) throw Fail{set_error(XMGN_ESTATE, "internal: out of tensor-map slots")};
     if (rows <= 0) throw Fail{set_error(XMGN_ESTATE, "internal: empty TMA input map")};
-    p.maps[next_map] = tmap_bf16(base, H, (uint64_t)rows, H, 64, 128);
+    p.maps[next_map] = tmap16(base, H, (uint64_t)rows, H, 64, 128, f16);
     return next_map++;
   }
 };
@@ -202,7 +206,6 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
   p.src = src;
   p.dst = dst;
   p.eps = ws->cfg.ln_eps;
-  { const char* d = getenv("XMGN_DBG"); p.dbg = d ? atoi(d) : 0; }
   const int n = pr.n;
   if (epi_writes_act(p.steps[n - 1])) throw Fail{set_error(XMGN_ESTATE, "internal: program ends writing ACT")};
   for (int s = 0; s < n; ++s) {
@@ -225,46 +228,19 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
   // weight maps
   const int NB = (ws->H < 256 ? ws->H : 256) / 2;   // B rows per CTA of a pair
   const long long r1 = (long long)ws->L * ws->S1 * ws->H, r2 = (long long)ws->L * ws->S2 * ws->H;
-  p.maps[0] = tmap_bf16(ws->wk1.p, ws->H, r1, ws->H, 64, NB);
-  p.maps[1] = ws->split ? tmap_bf16(ws->wk1.p + ws->wk1.lo, ws->H, r1, ws->H, 64, NB) : p.maps[0];
-  p.maps[2] = tmap_bf16(ws->wk2.p, 2 * ws->H, r2, 2 * ws->H, 64, NB);
-  p.maps[3] = ws->split ? tmap_bf16(ws->wk2.p + ws->wk2.lo, 2 * ws->H, r2, 2 * ws->H, 64, NB) : p.maps[2];
+  const bool f16 = ws->f16;
+  p.maps[0] = tmap16(ws->wk1.p, ws->H, r1, ws->H, 64, NB, f16);
+  p.maps[1] = ws->split ? tmap16(ws->wk1.p + ws->wk1.lo, ws->H, r1, ws->H, 64, NB, f16) : p.maps[0];
+  p.maps[2] = tmap16(ws->wk2.p, 2 * ws->H, r2, 2 * ws->H, 64, NB, f16);
+  p.maps[3] = ws->split ? tmap16(ws->wk2.p + ws->wk2.lo, 2 * ws->H, r2, 2 * ws->H, 64, NB, f16) : p.maps[2];
   const int pair_tiles = (M + 255) / 256;
   const int grid = 2 * (pair_tiles < ws->sms / 2 ? pair_tiles : ws->sms / 2);
   p.colsum = bwd ? ws->colsum : nullptr;
   if (bwd)
     XMGN_CUDA(cudaMemsetAsync(ws->colsum, 0, (size_t)grid * 4 * NV_MAX * ws->H * sizeof(float), st), "colsum zero");
-  // debug tracing (XMGN_TRACE=<scope name>): clock64 stamps of CTA 0, first launch only
-  static unsigned long long* trace_buf = nullptr;
-  static bool traced = false;
-  const char* tr = getenv("XMGN_TRACE");
-  const bool do_trace = tr && !traced && strcmp(tr, name) == 0;
-  if (do_trace) {
-    cudaMalloc(&trace_buf, 64 * 8 * 8);
-    cudaMemsetAsync(trace_buf, 0, 64 * 8 * 8, st);
-    p.trace = trace_buf;
-  }
   {
     ProfScope ps(name, st);
     launch_chain(ws->H, ws->split, ws->f16, bwd, p, grid, st);
-  }
-  if (do_trace) {
-    traced = true;
-    unsigned long long h[64 * 8];
-    cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    FILE* f = fopen("gpurun_out/trace.txt", "w");
-    if (f) {
-      fprintf(f, "# %s M=%d steps=%d: g, mma_start, mma_issued, epi_start, (split: ln_stats), epi_all_done, epi_end_w4, epi_end_w8, mma_after_acc_empty\n",
-              name, M, pr.n);
-      const unsigned long long t0 = h[0];
-      for (int g = 0; g < 64; ++g) {
-        fprintf(f, "%d", g);
-        for (int k = 0; k < 8; ++k) fprintf(f, " %lld", h[g * 8 + k] ? (long long)(h[g * 8 + k] - t0) : -1LL);
-        fprintf(f, "\n");
-      }
-      fclose(f);
-    }
   }
   XMGN_CUDA(cudaGetLastError(), "chain kernel launch");
 }
@@ -275,8 +251,8 @@ static int chain_grid(xmgn_workspace* ws, int M) {
 }
 
 static void set_a(xmgn_workspace* ws, Prog& pr, int slot, const BfBuf& b, long long rows, int width) {
-  pr.p.maps[slot] = map_rows(b.p, rows, width, 128);
-  pr.p.maps[slot + 1] = ws->split ? map_rows(b.p + b.lo, rows, width, 128) : pr.p.maps[slot];
+  pr.p.maps[slot] = map_rows(b.p, rows, width, 128, ws->f16);
+  pr.p.maps[slot + 1] = ws->split ? map_rows(b.p + b.lo, rows, width, 128, ws->f16) : pr.p.maps[slot];
 }
 
 static BfBuf at(const BfBuf& b, long long elem) { return BfBuf{b.p + elem, b.lo}; }
@@ -293,13 +269,14 @@ static void wgrad(xmgn_workspace* ws, const BfBuf& a0, const BfBuf& a1, int a_wi
   std::memset(&p, 0, sizeof(p));
   const BfBuf& a0r = a0.p ? a0 : b;
   const int aw = a0.p ? a_width : b_width;
-  p.a0 = tmap_bf16(a0r.p, aw, rows, aw, 64, 64);
-  p.a0lo = ws->split ? tmap_bf16(a0r.p + a0r.lo, aw, rows, aw, 64, 64) : p.a0;
+  const bool f16 = ws->f16;
+  p.a0 = tmap16(a0r.p, aw, rows, aw, 64, 64, f16);
+  p.a0lo = ws->split ? tmap16(a0r.p + a0r.lo, aw, rows, aw, 64, 64, f16) : p.a0;
   const BfBuf& a1r = a1.p ? a1 : a0r;
-  p.a1 = tmap_bf16(a1r.p, aw, rows, aw, 64, 64);
-  p.a1lo = ws->split ? tmap_bf16(a1r.p + a1r.lo, aw, rows, aw, 64, 64) : p.a1;
-  p.b = tmap_bf16(b.p, b_width, rows, b_width, 64, 64);
-  p.blo = ws->split ? tmap_bf16(b.p + b.lo, b_width, rows, b_width, 64, 64) : p.b;
+  p.a1 = tmap16(a1r.p, aw, rows, aw, 64, 64, f16);
+  p.a1lo = ws->split ? tmap16(a1r.p + a1r.lo, aw, rows, aw, 64, 64, f16) : p.a1;
+  p.b = tmap16(b.p, b_width, rows, b_width, 64, 64, f16);
+  p.blo = ws->split ? tmap16(b.p + b.lo, b_width, rows, b_width, 64, 64, f16) : p.b;
   p.a_split_tiles = a_split_tiles;
   p.b_col0 = b_col0;
   p.rows = (int)rows;
@@ -322,8 +299,8 @@ static void wgrad(xmgn_workspace* ws, const BfBuf& a0, const BfBuf& a1, int a_wi
   }
   XMGN_CUDA(cudaGetLastError(), "wgrad launch");
   const long long ld = (long long)(Hin + (p.ones_tile ? 128 : 0)) * H;
-  if (Hin > 0) launch_reduce_part(ws->part, S, (long long)Hin * H, ld, grad + dst, st);
-  if (p.ones_tile) launch_reduce_part(ws->part + (long long)Hin * H, S, H, ld, grad + bias_dst, st);
+  if (Hin > 0) launch_reduce_part(ws->part, S, (long long)Hin * H, ld, grad + dst, st, ws->d_scale + 1);
+  if (p.ones_tile) launch_reduce_part(ws->part + (long long)Hin * H, S, H, ld, grad + bias_dst, st, ws->d_scale + 1);
 }
 
 static void colsum_reduce(xmgn_workspace* ws, int blk, int l, float* grad, int grid_used, cudaStream_t st,
@@ -338,7 +315,7 @@ static void colsum_reduce(xmgn_workspace* ws, int blk, int l, float* grad, int g
     d.off[3] = Ly.b(l, blk, ws->m - 1);
     if (ws->m >= 2) d.off[4] = Ly.b(l, blk, ws->m - 2);
   }
-  launch_reduce_colsum(ws->colsum, grid_used, NV_MAX, ws->H, d, grad, st);
+  launch_reduce_colsum(ws->colsum, grid_used, NV_MAX, ws->H, d, grad, st, ws->d_scale + 1);
 }
 
 }  // namespace xmgn
@@ -412,6 +389,12 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
       ws->h_ck = bfalloc(ws, (size_t)L * NH);
       ws->a_ck = bfalloc(ws, (size_t)L * NH);
       for (int i = 0; i < 2; ++i) ws->h_buf[i] = (float*)dalloc(ws, NH * 4);
+      // BF16 operands (8-bit mantissa) need the edge residual stream and the aggregation in
+      // FP32 to stay inside north_star's 2e-2 x RMS at 15 layers (rung R1);
+      // FP16 operands meet it with the 16-bit stream
+      ws->e32_mode = cfg->precision == XMGN_PREC_BF16;
+      if (ws->e32_mode)
+        for (int i = 0; i < 2; ++i) ws->e32[i] = (float*)dalloc(ws, EH * 4);
       ws->P = bfalloc(ws, (size_t)L * 2 * NH);
       ws->Ge[0] = bfalloc(ws, EH);
       ws->Ge[1] = bfalloc(ws, EH);
@@ -423,19 +406,19 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
       ws->part_splits = 64;
       ws->part = (float*)dalloc(ws, (size_t)ws->part_splits * (2 * H + 128) * H * 4);
       ws->colsum = (float*)dalloc(ws, (size_t)ws->sms * 4 * NV_MAX * H * 4);
-      ws->d_flag = (int*)dalloc(ws, 4);
+      ws->d_amax = (unsigned int*)dalloc(ws, 4);
+      ws->d_scale = (float*)dalloc(ws, 2 * sizeof(float));
       // Opt-in (XMGN_Z1=1) memory-for-speed mode: z_1 checkpoints (+L x E x H x 2 bytes) let
       // the backward skip the first edge GEMM's recompute (edge bwd -5%).  Off by default: at
       // CFG4 on one GPU they would not leave room for the 62 GB of resident inputs.
+      // Explicitly requested: failing to allocate it is an error (ENOMEM), never a silent
+      // fall-back to the default mode.
       const char* z1env = getenv("XMGN_Z1");
-      if (!ws->split && z1env && atoi(z1env) == 1) {
-        size_t free_b = 0, total_b = 0;
-        cudaMemGetInfo(&free_b, &total_b);
-        const size_t need = (size_t)L * EH * sizeof(bf16);
-        if (free_b > need + ((size_t)8 << 30)) {
-          ws->z1_ck = bfalloc(ws, (size_t)L * EH);
-          ws->use_z1 = true;
-        }
+      if (z1env && atoi(z1env) == 1) {
+        if (ws->split)
+          throw Fail{set_error(XMGN_EUNSUPPORTED, "xmgn_workspace_create: XMGN_Z1=1 needs a 16-bit precision mode")};
+        ws->z1_ck = bfalloc(ws, (size_t)L * EH);
+        ws->use_z1 = true;
       }
     } catch (...) {
       xmgn_workspace_free(ws);
@@ -480,7 +463,7 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
     auto r1 = [&](int l, int slot) { return (l * ws->S1 + slot) * H; };
     auto r2 = [&](int l, int slot) { return (l * ws->S2 + slot) * H; };
     {  // P = h0 [W1e_s | W1e_d] for layer 1
-      Prog pr;
+      Prog pr(ws);
       set_a(ws, pr, 4, ws->h_ck, n0, H);
       for (int half = 0; half < 2; ++half) {
         Step& s = pr.add();
@@ -492,7 +475,7 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
       run_prog(ws, "chain_proj", pr, (int)n0, nullptr, nullptr, false, st);
     }
     auto Pl = [&](int li) { return ws->P.p + (long long)li * 2 * NH; };   // P of layer li + 1
-    int cur = 0;
+    int cur = 0, ce = 0;   // ping-pong indices of the FP32 node (and BF16-mode edge) streams
     for (int l = 1; l <= L; ++l) {
       const int li = l - 1;
       const int64_t nl = n_at(P, L, l), el = e_at(P, L, l);
@@ -502,7 +485,7 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
       BfBuf eck_prev = at(ws->e_ck, (long long)li * EH), hck_prev = at(ws->h_ck, (long long)li * NH);
       BfBuf ack = at(ws->a_ck, (long long)li * NH);
       {  // edge update (Eq. 1)
-        Prog pr;
+        Prog pr(ws);
         set_a(ws, pr, 4, eck_prev, el, H);
         for (int j = 0; j < m; ++j) {
           Step& s = pr.add();
@@ -515,23 +498,32 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
             if (ws->use_z1) { s.flags |= EF_STORE_Z; s.scr_z = ws->z1_ck.p + (long long)li * EH; }
           }
         }
-        // e^l = e^{l-1} + LN(..): the edge stream itself is 16-bit (checkpoint = next operand)
+        // e^l = e^{l-1} + LN(..): the edge stream itself is 16-bit (checkpoint = next operand);
+        // BF16 mode carries it in FP32 and writes the 16-bit operand / checkpoint beside it
         Step& s = pr.add();
         s.a_src = A_ACT; s.K = H; s.b_map = W1; s.b_row0 = r1(li, SL_EJT + m - 1);
         s.epi = EPI_LN_FWD; s.bias = params + Ly.b(li, 0, m);
         s.gamma = params + Ly.gamma(li, 0); s.beta = params + Ly.beta(li, 0);
-        s.flags = EF_RES16 | EF_STORE_BF;
-        s.res16 = eck_prev.p; s.res16_lo = eck_prev.lo;
-        if (!ws->split && el > 0) s.in_map = pr.in_map(eck_prev.p, el, H);   // residual e^{l-1} rows
+        if (ws->e32_mode) {
+          s.flags = EF_STORE_F32 | EF_STORE_BF;
+          s.f_in = l == 1 ? e0 : ws->e32[ce]; s.ld_in = H;
+          s.f_out = ws->e32[ce ^ 1]; s.ld_out = H;
+        } else {
+          s.flags = EF_RES16 | EF_STORE_BF;
+          s.res16 = eck_prev.p; s.res16_lo = eck_prev.lo;
+          if (!ws->split && el > 0) s.in_map = pr.in_map(eck_prev.p, el, H);   // residual e^{l-1} rows
+        }
         s.bf_out = eck_next.p; s.bf_lo = eck_next.lo;
         run_prog(ws, "chain_edge_fwd", pr, (int)el, dp.src, dp.dst, false, st);
       }
       // aggregation (Eq. 2) -> a^l (BF16 operand + checkpoint)
       { ProfScope ps("aggregate", st);
-      launch_aggregate(ws->f16, H, dp.off, eck_next.p, eck_next.lo, ack.p, ack.lo, (int)nl, st); }
+      if (ws->e32_mode) launch_aggregate32(H, dp.off, ws->e32[ce ^ 1], ack.p, (int)nl, st);
+      else launch_aggregate(ws->f16, H, dp.off, eck_next.p, eck_next.lo, ack.p, ack.lo, (int)nl, st); }
+      ce ^= 1;
       XMGN_CUDA(cudaGetLastError(), "aggregate launch");
       {  // node update (Eq. 3) [+ P for layer l+1]
-        Prog pr;
+        Prog pr(ws);
         set_a(ws, pr, 4, hck_prev, nl, H);
         set_a(ws, pr, 6, ack, nl, H);
         for (int j = 0; j < m; ++j) {
@@ -587,8 +579,9 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
     auto r2 = [&](int l, int slot) { return (l * ws->S2 + slot) * H; };
     launch_pack(ws->f16, params, ws->d_jobs, ws->njobs, st);
     // seed: dL/dh^L on owned rows (the loss mask of PAPER.md:197 is the prefix)
-    XMGN_CUDA(cudaMemcpyAsync(ws->Gh, grad_h_out, P.n_owned * H * sizeof(float), cudaMemcpyDeviceToDevice, st),
-              "seed copy");
+    // (times S, a power of two putting max|g| in [1, 2): every gradient that leaves is
+    // multiplied by 1/S again -- exact loss scaling of the 16-bit gradient streams)
+    launch_seed_scale(grad_h_out, (long long)P.n_owned * H, ws->d_amax, ws->Gh, ws->d_scale, st);
     const BfBuf none{};
     int gc = 0;   // which G_e buffer holds G_e^l
     for (int l = L; l >= 1; --l) {
@@ -649,7 +642,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         }
       };
       {  // node block backward
-        Prog pr;
+        Prog pr(ws);
         set_a(ws, pr, 4, hck, nl, H);
         set_a(ws, pr, 6, ack, nl, H);
         mlp_bwd(pr, 1);
@@ -667,7 +660,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
       }
       // P for layer l: the forward's checkpoint (no recompute)
       {  // edge block backward
-        Prog pr;
+        Prog pr(ws);
         set_a(ws, pr, 4, eck, el, H);
         mlp_bwd(pr, 0);
         Step& a = pr.add();   // G_e^{l-1} = G_e' + dZ0 W0[e rows]^T
@@ -690,7 +683,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
       launch_segsum(ws->f16, H, dp.off, dp.rev, ws->scrZ[0].p, ws->scrZ[0].lo, ws->D.p, ws->D.lo, (int)nprev, (int)el, st); }
       XMGN_CUDA(cudaGetLastError(), "segsum launch");
       {  // G_h^{l-1} = [rows < n_l] G_h + D [W_s | W_d]^T
-        Prog pr;
+        Prog pr(ws);
         set_a(ws, pr, 4, ws->D, nprev, 2 * H);
         Step& s = pr.add();
         s.a_src = A_TMA; s.a_map0 = 4; s.K = 2 * H; s.b_map = W2; s.b_row0 = r2(li, SL2_SD);
@@ -703,12 +696,12 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
     }
     const int64_t n0 = n_at(P, L, 0), e1 = e_at(P, L, 1);
     if (grad_h0) {
-      XMGN_CUDA(cudaMemcpyAsync(grad_h0, ws->Gh, n0 * H * sizeof(float), cudaMemcpyDeviceToDevice, st), "grad_h0");
+      launch_scale_copy(ws->Gh, n0 * H, ws->d_scale + 1, grad_h0, st);
       if (P.n_local > n0)
         XMGN_CUDA(cudaMemsetAsync(grad_h0 + n0 * H, 0, (P.n_local - n0) * H * sizeof(float), st), "grad_h0");
     }
     if (grad_e0) {
-      launch_to_f32(ws->f16, ws->Ge[gc].p, ws->Ge[gc].lo, grad_e0, e1 * H, st);
+      launch_to_f32(ws->f16, ws->Ge[gc].p, ws->Ge[gc].lo, grad_e0, e1 * H, st, ws->d_scale + 1);
       if (P.e_local > e1)
         XMGN_CUDA(cudaMemsetAsync(grad_e0 + e1 * H, 0, (P.e_local - e1) * H * sizeof(float), st), "grad_e0");
     }

@@ -26,23 +26,27 @@ inline EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// Row-major BF16 matrix [outer][inner] with row pitch `pitch_elems`; box
-// {box_inner (<=64 for SW128), box_outer (<=256)}; 128-byte swizzle; OOB rows
-// read as zero.
-inline CUtensorMap tmap_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_elems,
-                             uint32_t box_inner, uint32_t box_outer) {
+// Row-major 16-bit matrix [outer][inner] (FP16 if f16, else BF16) with row pitch
+// `pitch_elems`; box {box_inner (<=64 for SW128), box_outer (<=256)}; 128-byte
+// swizzle; OOB rows read as zero.
+inline CUtensorMap tmap16(const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_elems,
+                          uint32_t box_inner, uint32_t box_outer, bool f16) {
   CUtensorMap m;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {pitch_elems * 2};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+  CUresult r = encode_fn()(&m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ") inner=" +
                              std::to_string(inner) + " outer=" + std::to_string(outer));
   return m;
+}
+inline CUtensorMap tmap_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_elems,
+                             uint32_t box_inner, uint32_t box_outer) {
+  return tmap16(base, inner, outer, pitch_elems, box_inner, box_outer, false);
 }
 
 }  // namespace xmgn

@@ -15,7 +15,7 @@ from xmgn_inputs import tensors
 
 
 class Processor:
-    def __init__(self, bundle, H, L, m=2, precision=xmgn.PREC_BF16, device=0, parts=None, halo_depth=None,
+    def __init__(self, bundle, H, L, m=2, precision=xmgn.PREC_FP16, device=0, parts=None, halo_depth=None,
                  ln_eps=1e-5):
         torch.cuda.set_device(device)
         self.device = torch.device("cuda", device)

@@ -124,6 +124,7 @@ class Graph:
         _check(_lib.xmgn_load_graph(ctypes.byref(d), int(device), ctypes.byref(h)))
         self.handle = h
         self.n_parts = len(oo) - 1
+        self.device = int(device)
         self._keep = None
 
     @classmethod
@@ -158,12 +159,37 @@ class Graph:
         self.close()
 
 
-def model_cfg(hidden, layers, m=2, precision=PREC_BF16, ln_eps=1e-5):
+def model_cfg(hidden, layers, m=2, precision=PREC_FP16, ln_eps=1e-5):
     return ModelCfg(hidden, layers, m, precision, ln_eps)
 
 
 def param_count(cfg):
     return int(_lib.xmgn_param_count(ctypes.byref(cfg)))
+
+
+def _dev_f32(t, name, numel, device=None):
+    """Device pointer of a CUDA, float32, contiguous torch tensor holding at least
+    `numel` values (the library reads / writes exactly that many)."""
+    if t is None:
+        return None
+    if not hasattr(t, "data_ptr") or isinstance(t, np.ndarray):
+        raise TypeError(f"{name}: expected a CUDA torch tensor, got {type(t).__name__}")
+    if not t.is_cuda:
+        raise ValueError(f"{name}: tensor is on {t.device}, the library needs device memory")
+    if device is not None and t.device.index != device:
+        raise ValueError(f"{name}: tensor is on {t.device}, the graph lives on cuda:{device}")
+    if t.dtype != torch_float32():
+        raise TypeError(f"{name}: dtype {t.dtype}, expected torch.float32")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: tensor is not contiguous")
+    if t.numel() < numel:
+        raise ValueError(f"{name}: {t.numel()} values, the call needs {numel}")
+    return t.data_ptr()
+
+
+def torch_float32():
+    import torch
+    return torch.float32
 
 
 class Workspace:
@@ -174,17 +200,33 @@ class Workspace:
         h = _vp()
         _check(_lib.xmgn_workspace_create(graph.handle, ctypes.byref(cfg), ctypes.byref(h)))
         self.handle = h
+        self.n_params = param_count(cfg)
+        self._info = {}
 
     def nbytes(self):
         return int(_lib.xmgn_workspace_bytes(self.handle))
 
+    def _sizes(self, part):
+        if part not in self._info:
+            self._info[part] = self.graph.part_info(part)
+        i = self._info[part]
+        return i["n_owned"], i["n_local"], i["e_local"]
+
     def forward(self, part, params, h0, e0, h_out, stream=None):
-        _check(_lib.xmgn_processor_fwd(self.handle, int(part), _ptr(params), _ptr(h0), _ptr(e0), _ptr(h_out),
-                                       _stream(stream)))
+        no, nl, el = self._sizes(part)
+        H, dv = self.cfg.hidden, self.graph.device
+        _check(_lib.xmgn_processor_fwd(self.handle, int(part), _dev_f32(params, "params", self.n_params, dv),
+                                       _dev_f32(h0, "h0", nl * H, dv), _dev_f32(e0, "e0", el * H, dv),
+                                       _dev_f32(h_out, "h_out", no * H, dv), _stream(stream)))
 
     def backward(self, part, params, grad_h_out, grad_params, grad_h0=None, grad_e0=None, stream=None):
-        _check(_lib.xmgn_processor_bwd(self.handle, int(part), _ptr(params), _ptr(grad_h_out),
-                                       _ptr(grad_params), _ptr(grad_h0), _ptr(grad_e0), _stream(stream)))
+        no, nl, el = self._sizes(part)
+        H, dv = self.cfg.hidden, self.graph.device
+        _check(_lib.xmgn_processor_bwd(self.handle, int(part), _dev_f32(params, "params", self.n_params, dv),
+                                       _dev_f32(grad_h_out, "grad_h_out", no * H, dv),
+                                       _dev_f32(grad_params, "grad_params", self.n_params, dv),
+                                       _dev_f32(grad_h0, "grad_h0", nl * H, dv),
+                                       _dev_f32(grad_e0, "grad_e0", el * H, dv), _stream(stream)))
 
     def close(self):
         if getattr(self, "handle", None) and _lib is not None:
@@ -196,7 +238,7 @@ class Workspace:
 
 
 def check_finite(t, stream=None):
-    _check(_lib.xmgn_check_finite(_ptr(t), t.numel(), _stream(stream)))
+    _check(_lib.xmgn_check_finite(_dev_f32(t, "check_finite", t.numel()), t.numel(), _stream(stream)))
 
 
 class Comm:
@@ -214,7 +256,8 @@ class Comm:
         self.handle = h
 
     def grad_reduce(self, grad, stream=None):
-        _check(_lib.xmgn_grad_reduce(self.handle, _ptr(grad), grad.numel(), _stream(stream)))
+        _check(_lib.xmgn_grad_reduce(self.handle, _dev_f32(grad, "grad", grad.numel()), grad.numel(),
+                                     _stream(stream)))
 
     def close(self):
         if getattr(self, "handle", None):

@@ -8,12 +8,16 @@ import pytest
 import torch
 
 from xmgn_inputs import configs, geometry, graph, partition
-from gpu_util import (max_over_rms, oracle_full, oracle_probe, per_tensor_rel, rel_fro, run_gpu)
+from gpu_util import (max_over_rms, oracle_full, oracle_probe, per_tensor_rel, rel_fro, row_max_over_rms, run_gpu)
 
 pytestmark = pytest.mark.gpu
 
 FP32, BF16, FP16 = 1, 0, 2
 TAU = {FP32: 1e-4, BF16: 2e-2, FP16: 2e-2}
+# per-row gate on the input gradients (max over rows of the row error norm / the RMS row
+# norm, gpu_util.row_max_over_rms): a wrong, missing or double-counted row is O(1).  North_star
+# fixes no gradient tolerance; these are ~3-5x the per-row errors measured on B200.
+TAU_ROW = {FP32: 1e-3, BF16: 1e-1, FP16: 2e-2}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -23,7 +27,7 @@ def _lib():
     from paper_2411_17164_b200 import xmgn  # noqa: F401  (fails loudly if libxmgn.so is missing)
 
 
-def _check(res, ref, H, L, tau, m=2, inputs=True):
+def _check(res, ref, H, L, tau, m=2, inputs=True, tau_row=None):
     f = max_over_rms(res["h"], ref["h"])
     gw, name = per_tensor_rel(res["params"], ref["params"], H, L, m)
     assert f <= tau, f"forward max/RMS {f:.3e} > {tau}"
@@ -31,6 +35,11 @@ def _check(res, ref, H, L, tau, m=2, inputs=True):
     if inputs:
         assert rel_fro(res["h0"], ref["h0"]) <= tau
         assert rel_fro(res["e0"], ref["e0"]) <= tau
+        rh, re_ = row_max_over_rms(res["h0"], ref["h0"]), row_max_over_rms(res["e0"], ref["e0"])
+        tr = TAU_ROW[{1e-4: FP32}.get(tau, FP16)] if tau_row is None else tau_row
+        print(f"fwd max/RMS {f:.2e}  grad worst {name} {gw:.2e}  row h0 {rh:.2e}  row e0 {re_:.2e}")
+        assert rh <= tr, f"grad_h0 worst row {rh:.3e} > {tr}"
+        assert re_ <= tr, f"grad_e0 worst row {re_:.3e} > {tr}"
     return f, gw
 
 
@@ -62,7 +71,7 @@ def test_multiscale_partitioned_all_modes(prec):
     b = configs.custom((300, 1500), k=6, P=4, halo=3)
     res = run_gpu(b, 128, 3, prec)
     ref = oracle_full(b, 128, 3)
-    _check(res, ref, 128, 3, TAU[prec])
+    _check(res, ref, 128, 3, TAU[prec], tau_row=TAU_ROW[prec])
 
 
 @pytest.mark.parametrize("H", [256, 512])
@@ -71,7 +80,7 @@ def test_wide_hidden(H, prec):
     b = configs.custom((200, 900), k=6, P=2, halo=2, shape="car")
     res = run_gpu(b, H, 2, prec)
     ref = oracle_full(b, H, 2)
-    _check(res, ref, H, 2, TAU[prec])
+    _check(res, ref, H, 2, TAU[prec], tau_row=TAU_ROW[prec])
 
 
 def test_mlp_one_hidden_layer():
@@ -145,10 +154,13 @@ def test_check_finite_and_state_errors():
 
 
 @pytest.mark.slow
-def test_cfg2_full_forward_fp16():
-    """CFG2 at full size (100k points, 15 layers, H=128): every output row vs the oracle."""
+@pytest.mark.parametrize("prec", [FP16, BF16])
+def test_cfg2_full_forward_l15(prec):
+    """CFG2 at full size (100k points, 15 layers, H=128): every output row vs the oracle,
+    in the FP16 production mode and in the paper's BF16 -- north_star's
+    max|dh| <= 2e-2 x RMS(h_oracle) after 15 layers."""
     b = configs.load("cfg2")
-    res = run_gpu(b, 128, 15, FP16, want_inputs=False)
+    res = run_gpu(b, 128, 15, prec, want_inputs=False)
     import oracle
     from xmgn_inputs import tensors
     off, src = b["offsets"], b["sources"]
@@ -157,7 +169,53 @@ def test_cfg2_full_forward_fp16():
                        tensors.node_features(np.arange(N), 128).double().numpy(),
                        tensors.edge_features(np.arange(E), 128).double().numpy(), 128, 15)
     err = max_over_rms(res["h"], f["h"][-1])
-    assert err <= TAU[FP16], err
+    print(f"CFG2 L=15 prec={prec}: max/RMS {err:.3e}")
+    assert err <= TAU[prec], err
+
+
+@pytest.mark.parametrize("prec", [FP16, BF16])
+def test_mse_scaled_upstream_gradient(prec):
+    """The paper's loss is an MSE normalised over N x d, so dL/dh^L is
+    ~1e-7 per element -- below FP16's normal range (6.1e-5).  The backward scales its
+    seed by a power of two and unscales every gradient it returns (exact), so a 1e-7
+    upstream gradient gives 1e-7 x the unit-scale gradients, within the same tolerance.
+    15 layers, halo 15, 2 partitions."""
+    b = configs.custom((400, 2000), k=6, P=2, halo=15)
+    gs = 1e-7
+    res = run_gpu(b, 128, 15, prec, g_scale=gs)
+    ref = oracle_full(b, 128, 15, g_scale=gs)
+    for k in ("params", "h0", "e0"):
+        assert np.isfinite(res[k]).all(), k
+        assert np.abs(res[k]).max() > 0, k
+    _check(res, ref, 128, 15, TAU[prec], tau_row=TAU_ROW[prec])
+
+
+@pytest.mark.parametrize("prec", [FP32, FP16])
+def test_zero_variance_layernorm_rows(prec):
+    """with the last Linear of layer 1's edge and node MLPs set to
+    W = 0 and b = 0.25 (constant), every LayerNorm input row is constant: variance 0,
+    LN output = beta (eps > 0), and the backward's rstd = eps^-1/2 amplifies dY."""
+    H, L, m = 128, 3, 2
+    lay, _ = tensors_layout(H, L, m)
+
+    def fn(P):
+        P = P.copy()
+        for nm, l, blk, slot, o, shape, fan in lay:
+            n = int(np.prod(shape))
+            if l == 0 and nm == f"W{m + 1}":
+                P[o:o + n] = 0.0
+            if l == 0 and nm == f"b{m + 1}":
+                P[o:o + n] = 0.25
+        return P
+    b = configs.custom((300, 1500), k=6, P=4, halo=3)
+    res = run_gpu(b, H, L, prec, param_fn=fn)
+    ref = oracle_full(b, H, L, param_fn=fn)
+    _check(res, ref, H, L, TAU[prec], tau_row=TAU_ROW[prec])
+
+
+def tensors_layout(H, L, m):
+    from xmgn_inputs import tensors
+    return tensors.param_layout(H, L, m)
 
 
 @pytest.mark.slow
@@ -175,22 +233,73 @@ def test_cfg2_probe_gradients():
     for pnode in probes:
         o = oracle_probe(b, int(pnode), 128, 15)
         Gp = o["params"] if Gp is None else Gp + o["params"]
-        assert np.abs(res["h"][pnode] - o["h"]).max() <= TAU[FP16] * np.sqrt((res["h"] ** 2).mean())
+        assert np.abs(res["h"][pnode] - o["h"]).max() <= TAU[FP16] * np.sqrt((o["h"] ** 2).mean())
     gw, name = per_tensor_rel(res["params"], Gp, 128, 15)
     assert gw <= TAU[FP16], (gw, name)
 
 
+def _junction_probes(b, n_per_owner=4, seed=1):
+    """Probe rows around the points where four RCB partitions meet: for each owner-set
+    of size 4 that occurs within 2 hops of one node, that node's 2-hop neighbourhood,
+    n_per_owner rows of each of the 4 owners (partition-border rows by construction)."""
+    off, src, owner = b["offsets"], b["sources"], b["owner"]
+    N = len(off) - 1
+    dst = np.repeat(np.arange(N), np.diff(off))
+    m1 = (np.int64(1) << owner.astype(np.int64))
+    m = m1.copy()
+    np.bitwise_or.at(m, dst, m1[src])
+    m2 = m.copy()
+    np.bitwise_or.at(m2, dst, m[src])
+    bits = sum((m2 >> p) & 1 for p in range(int(owner.max()) + 1))
+    rng = np.random.default_rng(seed)
+    first = {}
+    for c in np.nonzero(bits == 4)[0]:
+        first.setdefault(int(m2[c]), int(c))
+    full = (1 << (int(owner.max()) + 1)) - 1
+    pair = next(((a, b2) for a in sorted(first) for b2 in sorted(first) if a & b2 == 0 and a | b2 == full), None)
+    assert pair is not None, "no two disjoint 4-partition junctions"
+    clusters = []
+    for mask in pair:
+        c = first[mask]
+        hop1 = src[off[c]:off[c + 1]]
+        near = np.unique(np.concatenate([[c], hop1] + [src[off[j]:off[j + 1]] for j in hop1]))
+        pick = []
+        for o in range(int(owner.max()) + 1):
+            cand = near[owner[near] == o]
+            if len(cand):
+                pick += list(rng.choice(cand, min(n_per_owner, len(cand)), replace=False))
+        clusters.append(np.array(sorted(pick)))
+    return clusters
+
+
 @pytest.mark.slow
 def test_cfg4_probe_forward():
-    """CFG4 (the bench workload: 2M-point 3-level cloud, 8 partitions, H=512,
-    L=15): one owned probe row per partition pair vs the oracle's 15-hop ball."""
+    """CFG4 (the bench workload: 2M-point 3-level cloud, 8 partitions, H=512, L=15, FP16,
+    the bench's launch configuration): 32 owned probe rows on the borders where four
+    partitions meet (two junctions: partitions 0-3 and 4-7), each vs the FP64 oracle on
+    the probes' 15-hop ball (itself a halo partition owning the probes).
+    Tolerance: 2e-2 x RMS of the oracle's own h^L over the probe rows."""
+    import oracle
+    from xmgn_inputs import tensors
     b = configs.load("cfg4")
+    clusters = _junction_probes(b)
+    probes = np.concatenate(clusters)
+    assert len(probes) >= 32 and len(set(b["owner"][probes])) == 8, (len(probes), set(b["owner"][probes]))
     res = run_gpu(b, 512, 15, FP16, want_inputs=False)
-    rms = np.sqrt((res["h"][b["owned"][:10000]] ** 2).mean())
-    N = len(b["offsets"]) - 1
-    for pnode in np.random.default_rng(1).choice(N, 1, replace=False):
-        o = oracle_probe(b, int(pnode), 512, 15, with_grad=False)
-        assert np.abs(res["h"][pnode] - o["h"]).max() <= TAU[FP16] * rms
+    P = tensors.params(512, 15).double().numpy()
+    got, ref = [], []
+    for c in clusters:
+        lg = oracle.local_graph(b["offsets"], b["sources"], c, 15)
+        h0 = tensors.node_features(lg["gid"], 512).double().numpy()
+        e0 = tensors.edge_features(lg["edge_gid"], 512).double().numpy()
+        f = oracle.forward(lg["offsets"], lg["sources"], P, h0, e0, 512, 15)
+        ref.append(f["h"][-1][:lg["n_owned"]])
+        got.append(res["h"][lg["gid"][:lg["n_owned"]]])
+    got, ref = np.concatenate(got), np.concatenate(ref)
+    rms = np.sqrt((ref ** 2).mean())
+    err = np.abs(got - ref).max(axis=1) / rms
+    print(f"CFG4 {len(err)} probes: max/RMS worst {err.max():.3e} median {np.median(err):.3e}")
+    assert err.max() <= TAU[FP16], err
 
 
 def _hand_bundle(offsets, sources, owner, P, halo):
@@ -213,7 +322,7 @@ def test_degenerate_graphs(prec):
     b = _hand_bundle(offsets, sources, [0, 0, 1, 1, 2, 2, 2], 3, 2)
     res = run_gpu(b, 128, 2, prec)
     ref = oracle_full(b, 128, 2)
-    _check(res, ref, 128, 2, TAU[prec])
+    _check(res, ref, 128, 2, TAU[prec], tau_row=TAU_ROW[prec])
 
 
 def test_single_partial_tile_many_partitions():
@@ -237,7 +346,7 @@ def test_cfg4_probe_gradients():
     mask[probe] = 1.0
     res = run_gpu(b, 512, 15, FP16, g_rows=mask, want_inputs=False)
     o = oracle_probe(b, probe, 512, 15)
-    rms = np.sqrt((res["h"][b["owned"][:10000]] ** 2).mean())
+    rms = np.sqrt((o["h"] ** 2).mean())      # the oracle's own row scale
     assert np.abs(res["h"][probe] - o["h"]).max() <= TAU[FP16] * rms
     gw, name = per_tensor_rel(res["params"], o["params"], 512, 15)
     assert gw <= TAU[FP16], (gw, name)
@@ -246,8 +355,18 @@ def test_cfg4_probe_gradients():
 def test_z1_checkpoint_mode(monkeypatch):
     """Opt-in XMGN_Z1=1: the forward keeps z_1 and the backward replaces the first edge
     GEMM's recompute by a K = 0 step that reloads it; same parity bound as the default."""
-    monkeypatch.setenv("XMGN_Z1", "1")
+    from paper_2411_17164_b200.processor import Processor
     b = configs.custom((300, 1500), k=6, P=4, halo=3)
+    monkeypatch.delenv("XMGN_Z1", raising=False)
+    pr = Processor(b, 512, 3)
+    base = pr.ws.nbytes()
+    emax = max(pr.info[p]["e_local"] for p in pr.parts)
+    pr.close()
+    monkeypatch.setenv("XMGN_Z1", "1")
+    pr = Processor(b, 512, 3)
+    grown = pr.ws.nbytes() - base
+    pr.close()
+    assert grown >= 3 * emax * 512 * 2, (grown, emax)     # the z_1 checkpoints exist: Z1 mode is on
     res = run_gpu(b, 512, 3, FP16)
     ref = oracle_full(b, 512, 3)
     _check(res, ref, 512, 3, TAU[FP16])
