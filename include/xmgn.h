@@ -130,6 +130,14 @@ size_t xmgn_param_count(const xmgn_model_cfg* cfg);
  * fall-back); XMGN_Z1=1 with the FP32 check mode is EUNSUPPORTED.
  * xmgn_workspace_bytes reports the total allocated.                          */
 xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_model_cfg* cfg, xmgn_workspace** out);
+/* Inference workspace (Sec. III-D: "Inference is performed
+ * independently on each partition. Predictions on halo nodes are discarded"):
+ * xmgn_processor_fwd runs exactly the training forward (bitwise identical
+ * h_out) but keeps no per-layer checkpoints -- the 16-bit edge / node operands,
+ * aggregates and pre-projections are ping-ponged, about two layers of activation
+ * memory instead of L+1, so far fewer (larger) partitions fit a GPU
+ * ("significantly smaller" P_infer).  xmgn_processor_bwd on it returns ESTATE. */
+xmgn_status xmgn_workspace_create_infer(const xmgn_graph* g, const xmgn_model_cfg* cfg, xmgn_workspace** out);
 size_t xmgn_workspace_bytes(const xmgn_workspace* ws);
 void xmgn_workspace_free(xmgn_workspace* ws);
 
@@ -157,7 +165,19 @@ xmgn_status xmgn_check_finite(const float* dev, size_t n, void* stream);
 xmgn_status xmgn_comm_unique_id(uint8_t id[128]);
 xmgn_status xmgn_comm_init(const uint8_t id[128], int nranks, int rank, int cuda_device, xmgn_comm** out);
 xmgn_status xmgn_grad_reduce(xmgn_comm* comm, float* grad_params, size_t count, void* stream);
+/* Inference gather ("the remaining predictions are aggregated on
+ * the master rank to reconstruct the full-domain output"): every rank sends
+ * send_rows x row_elems FP32 values (device) to rank 0 with NCCL point-to-point
+ * calls on `stream`; rank 0 receives rank r's block at
+ * recv + row_elems * sum_{q<r} recv_rows[q] (recv_rows: host [nranks], rank 0
+ * only, recv_rows[0] == its own send_rows; other ranks may pass NULL).        */
+xmgn_status xmgn_gather_rows(xmgn_comm* comm, const float* send, int64_t send_rows, int64_t row_elems, float* recv,
+                             const int64_t* recv_rows, void* stream);
 void xmgn_comm_destroy(xmgn_comm* comm);
+/* dst[idx[i], :] = src[i, :] for i < n, rows of row_elems FP32 (device arrays;
+ * idx int64 device).  Places gathered owned rows at their global ids.        */
+xmgn_status xmgn_scatter_rows(const float* src, const int64_t* idx, int64_t n, int64_t row_elems, float* dst,
+                              void* stream);
 
 /* ------------------------------------------------------------------ diagnostics
  * C[M,N] FP32 = A * B^T on tcgen05 with A [M,K] (a_mn_major=0) or [K,M] (=1)

@@ -19,6 +19,10 @@ struct Nccl {
   decltype(&ncclAllReduce) allReduce = nullptr;
   decltype(&ncclCommDestroy) commDestroy = nullptr;
   decltype(&ncclGetErrorString) getErrorString = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
   bool ok = false;
 };
 const Nccl& nccl() {
@@ -32,7 +36,12 @@ const Nccl& nccl() {
     r.allReduce = (decltype(r.allReduce))dlsym(h, "ncclAllReduce");
     r.commDestroy = (decltype(r.commDestroy))dlsym(h, "ncclCommDestroy");
     r.getErrorString = (decltype(r.getErrorString))dlsym(h, "ncclGetErrorString");
-    r.ok = r.getUniqueId && r.commInitRank && r.allReduce && r.commDestroy && r.getErrorString;
+    r.send = (decltype(r.send))dlsym(h, "ncclSend");
+    r.recv = (decltype(r.recv))dlsym(h, "ncclRecv");
+    r.groupStart = (decltype(r.groupStart))dlsym(h, "ncclGroupStart");
+    r.groupEnd = (decltype(r.groupEnd))dlsym(h, "ncclGroupEnd");
+    r.ok = r.getUniqueId && r.commInitRank && r.allReduce && r.commDestroy && r.getErrorString && r.send && r.recv &&
+           r.groupStart && r.groupEnd;
     return r;
   }();
   return n;
@@ -41,7 +50,7 @@ const Nccl& nccl() {
 
 struct xmgn_comm {
   ncclComm_t comm = nullptr;
-  int device = 0;
+  int device = 0, nranks = 1, rank = 0;
 };
 
 using namespace xmgn;
@@ -74,6 +83,8 @@ extern "C" xmgn_status xmgn_comm_init(const uint8_t id[128], int nranks, int ran
   std::memcpy(&u, id, 128);
   auto* c = new xmgn_comm();
   c->device = cuda_device;
+  c->nranks = nranks;
+  c->rank = rank;
   xmgn_status s = nccl_status(nccl().commInitRank(&c->comm, nranks, u, rank), "xmgn_comm_init");
   if (s != XMGN_OK) { delete c; return s; }
   *out = c;
@@ -87,6 +98,45 @@ extern "C" xmgn_status xmgn_grad_reduce(xmgn_comm* c, float* grad, size_t count,
   if (e != cudaSuccess) return cuda_status(e, "xmgn_grad_reduce: cudaSetDevice");
   return nccl_status(nccl().allReduce(grad, grad, count, ncclFloat32, ncclSum, c->comm, (cudaStream_t)stream),
                      "xmgn_grad_reduce");
+}
+
+// Inference gather ("the remaining predictions are aggregated on the master
+// rank"): point-to-point sends of each rank's owned rows to rank 0, one NCCL group.
+extern "C" xmgn_status xmgn_gather_rows(xmgn_comm* c, const float* send, int64_t send_rows, int64_t row_elems,
+                                        float* recv, const int64_t* recv_rows, void* stream) {
+  if (!c || send_rows < 0 || row_elems <= 0 || (send_rows && !send))
+    return set_error(XMGN_EINVAL, "xmgn_gather_rows: bad arguments (send_rows=%lld row_elems=%lld)",
+                     (long long)send_rows, (long long)row_elems);
+  if (c->rank == 0 && (!recv_rows || !recv))
+    return set_error(XMGN_EINVAL, "xmgn_gather_rows: rank 0 needs recv and recv_rows");
+  if (c->rank == 0 && recv_rows[0] != send_rows)
+    return set_error(XMGN_EINVAL, "xmgn_gather_rows: recv_rows[0]=%lld but rank 0 sends %lld rows",
+                     (long long)recv_rows[0], (long long)send_rows);
+  XMGN_NEED_NCCL("xmgn_gather_rows");
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return cuda_status(e, "xmgn_gather_rows: cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t re = (size_t)row_elems;
+  if (c->rank == 0) {
+    if (send_rows) {
+      e = cudaMemcpyAsync(recv, send, (size_t)send_rows * re * sizeof(float), cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) return cuda_status(e, "xmgn_gather_rows: local copy");
+    }
+    xmgn_status s = nccl_status(nccl().groupStart(), "xmgn_gather_rows");
+    if (s != XMGN_OK) return s;
+    size_t at = (size_t)recv_rows[0] * re;
+    for (int r = 1; r < c->nranks && s == XMGN_OK; ++r) {
+      if (recv_rows[r] < 0) s = set_error(XMGN_EINVAL, "xmgn_gather_rows: recv_rows[%d] < 0", r);
+      else if (recv_rows[r])
+        s = nccl_status(nccl().recv(recv + at, (size_t)recv_rows[r] * re, ncclFloat32, r, c->comm, st),
+                        "xmgn_gather_rows: recv");
+      at += (size_t)(recv_rows[r] > 0 ? recv_rows[r] : 0) * re;
+    }
+    xmgn_status s2 = nccl_status(nccl().groupEnd(), "xmgn_gather_rows");
+    return s != XMGN_OK ? s : s2;
+  }
+  if (!send_rows) return XMGN_OK;
+  return nccl_status(nccl().send(send, (size_t)send_rows * re, ncclFloat32, 0, c->comm, st), "xmgn_gather_rows: send");
 }
 
 extern "C" void xmgn_comm_destroy(xmgn_comm* c) {

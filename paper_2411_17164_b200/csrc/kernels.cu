@@ -444,6 +444,16 @@ __global__ void k_scale_copy(const float* __restrict__ in, long long n, const fl
     out[i] = in[i] * u;
 }
 
+// dst[idx[i]] row = src[i] row (row_elems % 4 == 0 -> float4 path)
+__global__ void k_scatter_rows(const float* __restrict__ src, const long long* __restrict__ idx, long long n,
+                               long long row_elems, float* __restrict__ dst) {
+  const long long tot = n * row_elems;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / row_elems, c = t % row_elems;
+    dst[idx[i] * row_elems + c] = src[t];
+  }
+}
+
 __global__ void k_nonfinite(const float* __restrict__ x, long long n, int* __restrict__ flag) {
   int bad = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -558,6 +568,13 @@ void launch_reduce_colsum(const float* part, int nblk, int nv, int H, ColsumDst 
                           const float* inv) {
   count_launch();
   k_reduce_colsum<<<(nv * H + 255) / 256, 256, 0, st>>>(part, nblk, nv, H, d, grad, inv);
+}
+void launch_scatter_rows(const float* src, const long long* idx, long long n, long long row_elems, float* dst,
+                         cudaStream_t st) {
+  if (n <= 0) return;
+  count_launch();
+  const int blocks = (int)std::min<long long>((n * row_elems + 255) / 256, 148 * 16);
+  k_scatter_rows<<<blocks, 256, 0, st>>>(src, idx, n, row_elems, dst);
 }
 void launch_nonfinite(const float* x, long long n, int* flag, cudaStream_t st) {
   count_launch();

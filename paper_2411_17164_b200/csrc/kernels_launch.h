@@ -32,6 +32,8 @@ void launch_reduce_part(const float* part, int S, long long n, long long ld, flo
                         const float* inv = nullptr);
 void launch_reduce_colsum(const float* part, int nblk, int nv, int H, ColsumDst d, float* grad, cudaStream_t st,
                           const float* inv = nullptr);
+void launch_scatter_rows(const float* src, const long long* idx, long long n, long long row_elems, float* dst,
+                         cudaStream_t st);
 void launch_nonfinite(const float* x, long long n, int* flag, cudaStream_t st);
 // profiling (processor.cu): every kernel launch of the library is counted;
 // when enabled, named launch scopes are bracketed by CUDA events on their stream.

@@ -68,6 +68,9 @@ struct xmgn_workspace {
   unsigned int* d_amax = nullptr;  // max|g| bits of the current backward's seed
   float* d_scale = nullptr;        // {S, 1/S}: the backward's power-of-two loss scale
   int last_fwd = -1;
+  bool infer = false;   // inference workspace: forward only, per-layer buffers ping-ponged
+  // checkpoint slot of layer l's tensors (training: one per layer; inference: ping-pong)
+  long long ck(int l) const { return infer ? (l & 1) : l; }
 };
 
 namespace xmgn {
@@ -328,7 +331,8 @@ extern "C" size_t xmgn_param_count(const xmgn_model_cfg* c) {
   return (size_t)Ly.count();
 }
 
-extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_model_cfg* cfg, xmgn_workspace** out) {
+static xmgn_status workspace_create(const xmgn_graph* g, const xmgn_model_cfg* cfg, xmgn_workspace** out,
+                                    bool infer) {
   return guarded("xmgn_workspace_create", [&]() -> xmgn_status {
     if (!g || !cfg || !out) return set_error(XMGN_EINVAL, "xmgn_workspace_create: null argument");
     *out = nullptr;
@@ -352,6 +356,7 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
     try {
       ws->g = g;
       ws->cfg = *cfg;
+      ws->infer = infer;
       ws->dev = g->device;
       ws->H = H; ws->L = L; ws->m = m;
       ws->split = cfg->precision == XMGN_PREC_FP32_CHECK;
@@ -385,9 +390,12 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
       ws->njobs = (int)jobs.size();
       ws->d_jobs = (PackJob*)dalloc(ws, jobs.size() * sizeof(PackJob));
       XMGN_CUDA(cudaMemcpy(ws->d_jobs, jobs.data(), jobs.size() * sizeof(PackJob), cudaMemcpyHostToDevice), "upload");
-      ws->e_ck = bfalloc(ws, (size_t)(L + 1) * EH);
-      ws->h_ck = bfalloc(ws, (size_t)L * NH);
-      ws->a_ck = bfalloc(ws, (size_t)L * NH);
+      // training keeps every layer's 16-bit operands (activation checkpoints);
+      // inference ping-pongs them: ~2 layers of activation memory
+      const int ckL = infer ? 2 : L;
+      ws->e_ck = bfalloc(ws, (size_t)(infer ? 2 : L + 1) * EH);
+      ws->h_ck = bfalloc(ws, (size_t)ckL * NH);
+      ws->a_ck = bfalloc(ws, (size_t)(infer ? 1 : L) * NH);
       for (int i = 0; i < 2; ++i) ws->h_buf[i] = (float*)dalloc(ws, NH * 4);
       // BF16 operands (8-bit mantissa) need the edge residual stream and the aggregation in
       // FP32 to stay inside north_star's 2e-2 x RMS at 15 layers (rung R1);
@@ -395,17 +403,19 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
       ws->e32_mode = cfg->precision == XMGN_PREC_BF16;
       if (ws->e32_mode)
         for (int i = 0; i < 2; ++i) ws->e32[i] = (float*)dalloc(ws, EH * 4);
-      ws->P = bfalloc(ws, (size_t)L * 2 * NH);
-      ws->Ge[0] = bfalloc(ws, EH);
-      ws->Ge[1] = bfalloc(ws, EH);
-      ws->Gh = (float*)dalloc(ws, NH * 4);
-      ws->Ga = bfalloc(ws, NH);
-      for (int j = 0; j < m; ++j) { ws->scrA[j] = bfalloc(ws, RH); ws->scrS[j] = bfalloc(ws, RH); }
-      for (int j = 0; j <= m; ++j) ws->scrZ[j] = bfalloc(ws, RH);
-      ws->D = bfalloc(ws, 2 * NH);
-      ws->part_splits = 64;
-      ws->part = (float*)dalloc(ws, (size_t)ws->part_splits * (2 * H + 128) * H * 4);
-      ws->colsum = (float*)dalloc(ws, (size_t)ws->sms * 4 * NV_MAX * H * 4);
+      ws->P = bfalloc(ws, (size_t)ckL * 2 * NH);
+      if (!infer) {
+        ws->Ge[0] = bfalloc(ws, EH);
+        ws->Ge[1] = bfalloc(ws, EH);
+        ws->Gh = (float*)dalloc(ws, NH * 4);
+        ws->Ga = bfalloc(ws, NH);
+        for (int j = 0; j < m; ++j) { ws->scrA[j] = bfalloc(ws, RH); ws->scrS[j] = bfalloc(ws, RH); }
+        for (int j = 0; j <= m; ++j) ws->scrZ[j] = bfalloc(ws, RH);
+        ws->D = bfalloc(ws, 2 * NH);
+        ws->part_splits = 64;
+        ws->part = (float*)dalloc(ws, (size_t)ws->part_splits * (2 * H + 128) * H * 4);
+        ws->colsum = (float*)dalloc(ws, (size_t)ws->sms * 4 * NV_MAX * H * 4);
+      }
       ws->d_amax = (unsigned int*)dalloc(ws, 4);
       ws->d_scale = (float*)dalloc(ws, 2 * sizeof(float));
       // Opt-in (XMGN_Z1=1) memory-for-speed mode: z_1 checkpoints (+L x E x H x 2 bytes) let
@@ -414,7 +424,7 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
       // Explicitly requested: failing to allocate it is an error (ENOMEM), never a silent
       // fall-back to the default mode.
       const char* z1env = getenv("XMGN_Z1");
-      if (z1env && atoi(z1env) == 1) {
+      if (!infer && z1env && atoi(z1env) == 1) {
         if (ws->split)
           throw Fail{set_error(XMGN_EUNSUPPORTED, "xmgn_workspace_create: XMGN_Z1=1 needs a 16-bit precision mode")};
         ws->z1_ck = bfalloc(ws, (size_t)L * EH);
@@ -427,6 +437,14 @@ extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_mod
     *out = ws;
     return XMGN_OK;
   });
+}
+
+extern "C" xmgn_status xmgn_workspace_create(const xmgn_graph* g, const xmgn_model_cfg* cfg, xmgn_workspace** out) {
+  return workspace_create(g, cfg, out, false);
+}
+extern "C" xmgn_status xmgn_workspace_create_infer(const xmgn_graph* g, const xmgn_model_cfg* cfg,
+                                                   xmgn_workspace** out) {
+  return workspace_create(g, cfg, out, true);
 }
 
 extern "C" size_t xmgn_workspace_bytes(const xmgn_workspace* ws) { return ws ? ws->bytes : 0; }
@@ -474,16 +492,16 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
       }
       run_prog(ws, "chain_proj", pr, (int)n0, nullptr, nullptr, false, st);
     }
-    auto Pl = [&](int li) { return ws->P.p + (long long)li * 2 * NH; };   // P of layer li + 1
+    auto Pl = [&](int li) { return ws->P.p + ws->ck(li) * 2 * NH; };   // P of layer li + 1
     int cur = 0, ce = 0;   // ping-pong indices of the FP32 node (and BF16-mode edge) streams
     for (int l = 1; l <= L; ++l) {
       const int li = l - 1;
       const int64_t nl = n_at(P, L, l), el = e_at(P, L, l);
       const float* h_in = l == 1 ? h0 : ws->h_buf[cur];
-      BfBuf eck_next = at(ws->e_ck, (long long)l * EH);
+      BfBuf eck_next = at(ws->e_ck, ws->ck(l) * EH);
       float* hn = l == L ? h_out : ws->h_buf[cur ^ 1];
-      BfBuf eck_prev = at(ws->e_ck, (long long)li * EH), hck_prev = at(ws->h_ck, (long long)li * NH);
-      BfBuf ack = at(ws->a_ck, (long long)li * NH);
+      BfBuf eck_prev = at(ws->e_ck, ws->ck(li) * EH), hck_prev = at(ws->h_ck, ws->ck(li) * NH);
+      BfBuf ack = at(ws->a_ck, ws->infer ? 0 : (long long)li * NH);
       {  // edge update (Eq. 1)
         Prog pr(ws);
         set_a(ws, pr, 4, eck_prev, el, H);
@@ -541,7 +559,7 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
         s.flags = EF_STORE_F32;
         if (l < L) {
           s.flags |= EF_STORE_BF | EF_WRITE_ACT;
-          s.bf_out = ws->h_ck.p + (long long)l * NH; s.bf_lo = ws->h_ck.lo;
+          s.bf_out = ws->h_ck.p + ws->ck(l) * NH; s.bf_lo = ws->h_ck.lo;
           for (int half = 0; half < 2; ++half) {
             Step& q = pr.add();
             q.a_src = A_ACT; q.K = H; q.b_map = W1; q.b_row0 = r1(l, half ? SL_PDT : SL_PST);
@@ -563,6 +581,8 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
   return guarded("xmgn_processor_bwd", [&]() -> xmgn_status {
     if (!ws || !params || !grad_h_out || !grad_params)
       return set_error(XMGN_EINVAL, "xmgn_processor_bwd: null argument");
+    if (ws->infer)
+      return set_error(XMGN_ESTATE, "xmgn_processor_bwd: inference workspace (no checkpoints; use xmgn_workspace_create)");
     if (part != ws->last_fwd)
       return set_error(XMGN_ESTATE, "xmgn_processor_bwd: part=%d but the workspace holds the forward of part %d",
                        part, ws->last_fwd);
@@ -705,6 +725,18 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
       if (P.e_local > e1)
         XMGN_CUDA(cudaMemsetAsync(grad_e0 + e1 * H, 0, (P.e_local - e1) * H * sizeof(float), st), "grad_e0");
     }
+    return XMGN_OK;
+  });
+}
+
+extern "C" xmgn_status xmgn_scatter_rows(const float* src, const int64_t* idx, int64_t n, int64_t row_elems,
+                                         float* dst, void* stream) {
+  return guarded("xmgn_scatter_rows", [&]() -> xmgn_status {
+    if (n < 0 || row_elems <= 0 || (n && (!src || !idx || !dst)))
+      return set_error(XMGN_EINVAL, "xmgn_scatter_rows: bad arguments (n=%lld row_elems=%lld)", (long long)n,
+                       (long long)row_elems);
+    launch_scatter_rows(src, (const long long*)idx, n, row_elems, dst, (cudaStream_t)stream);
+    XMGN_CUDA(cudaGetLastError(), "xmgn_scatter_rows launch");
     return XMGN_OK;
   });
 }

@@ -16,14 +16,14 @@ from xmgn_inputs import tensors
 
 class Processor:
     def __init__(self, bundle, H, L, m=2, precision=xmgn.PREC_FP16, device=0, parts=None, halo_depth=None,
-                 ln_eps=1e-5):
+                 ln_eps=1e-5, infer=False):
         torch.cuda.set_device(device)
         self.device = torch.device("cuda", device)
         self.H, self.L, self.m = H, L, m
         depth = L if halo_depth is None else halo_depth
         self.graph = xmgn.Graph.from_bundle(bundle, depth, device)
         self.cfg = xmgn.model_cfg(H, L, m, precision, ln_eps)
-        self.ws = xmgn.Workspace(self.graph, self.cfg)
+        self.ws = xmgn.Workspace(self.graph, self.cfg, infer=infer)
         self.parts = list(range(self.graph.n_parts)) if parts is None else list(parts)
         self.info = {p: self.graph.export(p) for p in self.parts}
         self.n_params = xmgn.param_count(self.cfg)
@@ -64,6 +64,16 @@ class Processor:
             outs.append(self.forward(p, params, h0, e0, stream))
             self.backward(p, params, g, grad_params, stream=stream)
         return outs
+
+    def infer(self, params, inputs, stream=None):
+        """Forward of every local partition; returns (rows [sum n_owned, H], global ids) of the
+        owned rows in partition order -- halo predictions are never returned."""
+        outs, gids = [], []
+        for p in self.parts:
+            h0, e0 = inputs[p][0], inputs[p][1]
+            outs.append(self.forward(p, params, h0, e0, stream))
+            gids.append(self.info[p]["gid"][:self.info[p]["n_owned"]])
+        return torch.cat(outs), np.concatenate(gids)
 
     def close(self):
         self.ws.close()

@@ -60,6 +60,7 @@ _sig("xmgn_export_part", _i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp])
 _sig("xmgn_free_graph", None, [_vp])
 _sig("xmgn_param_count", _sz, [ctypes.POINTER(ModelCfg)])
 _sig("xmgn_workspace_create", _i32, [_vp, ctypes.POINTER(ModelCfg), ctypes.POINTER(_vp)])
+_sig("xmgn_workspace_create_infer", _i32, [_vp, ctypes.POINTER(ModelCfg), ctypes.POINTER(_vp)])
 _sig("xmgn_workspace_bytes", _sz, [_vp])
 _sig("xmgn_workspace_free", None, [_vp])
 _sig("xmgn_processor_fwd", _i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp])
@@ -69,6 +70,8 @@ _sig("xmgn_comm_unique_id", _i32, [ctypes.c_char_p])
 _sig("xmgn_comm_init", _i32, [ctypes.c_char_p, _i32, _i32, _i32, ctypes.POINTER(_vp)])
 _sig("xmgn_grad_reduce", _i32, [_vp, _vp, _sz, _vp])
 _sig("xmgn_comm_destroy", None, [_vp])
+_sig("xmgn_gather_rows", _i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp])
+_sig("xmgn_scatter_rows", _i32, [_vp, _vp, _i64, _i64, _vp, _vp])
 _sig("xmgn_selftest_gemm", _i32, [_i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp])
 _sig("xmgn_launch_count", ctypes.c_longlong, [])
 _sig("xmgn_profile_enable", _i32, [_i32])
@@ -76,9 +79,11 @@ _sig("xmgn_profile_collect", _i32, [ctypes.c_char_p, _sz, ctypes.POINTER(ctypes.
                                     ctypes.POINTER(ctypes.c_longlong), _i32, ctypes.POINTER(_i32)])
 
 EXPORTS = ["xmgn_last_error", "xmgn_version", "xmgn_load_graph", "xmgn_part_info_get", "xmgn_export_part",
-           "xmgn_free_graph", "xmgn_param_count", "xmgn_workspace_create", "xmgn_workspace_bytes",
+           "xmgn_free_graph", "xmgn_param_count", "xmgn_workspace_create", "xmgn_workspace_create_infer",
+           "xmgn_workspace_bytes",
            "xmgn_workspace_free", "xmgn_processor_fwd", "xmgn_processor_bwd", "xmgn_check_finite",
-           "xmgn_comm_unique_id", "xmgn_comm_init", "xmgn_grad_reduce", "xmgn_comm_destroy",
+           "xmgn_comm_unique_id", "xmgn_comm_init", "xmgn_grad_reduce", "xmgn_comm_destroy", "xmgn_gather_rows",
+           "xmgn_scatter_rows",
            "xmgn_selftest_gemm", "xmgn_launch_count", "xmgn_profile_enable", "xmgn_profile_collect"]
 
 
@@ -195,10 +200,12 @@ def torch_float32():
 class Workspace:
     """xmgn_workspace_create / processor_fwd / processor_bwd for one GPU."""
 
-    def __init__(self, graph, cfg):
-        self.graph, self.cfg = graph, cfg
+    def __init__(self, graph, cfg, infer=False):
+        """infer=True: xmgn_workspace_create_infer (forward only, no checkpoints)."""
+        self.graph, self.cfg, self.infer = graph, cfg, infer
         h = _vp()
-        _check(_lib.xmgn_workspace_create(graph.handle, ctypes.byref(cfg), ctypes.byref(h)))
+        create = _lib.xmgn_workspace_create_infer if infer else _lib.xmgn_workspace_create
+        _check(create(graph.handle, ctypes.byref(cfg), ctypes.byref(h)))
         self.handle = h
         self.n_params = param_count(cfg)
         self._info = {}
@@ -259,10 +266,34 @@ class Comm:
         _check(_lib.xmgn_grad_reduce(self.handle, _dev_f32(grad, "grad", grad.numel()), grad.numel(),
                                      _stream(stream)))
 
+    def gather_rows(self, send, recv=None, recv_rows=None, stream=None):
+        """Rank 0 receives every rank's rows (send: [rows, W] CUDA float32) into recv in rank
+        order; recv_rows: per-rank row counts (rank 0 only)."""
+        W = send.shape[1] if send.dim() == 2 else 1
+        rr = None
+        if recv_rows is not None:
+            rr = np.ascontiguousarray(recv_rows, dtype=np.int64)
+            need = int(rr.sum()) * W
+        _check(_lib.xmgn_gather_rows(self.handle, _dev_f32(send, "send", send.numel()), send.shape[0], W,
+                                     _dev_f32(recv, "recv", need) if recv is not None else None,
+                                     rr.ctypes.data if rr is not None else None, _stream(stream)))
+
     def close(self):
         if getattr(self, "handle", None):
             _lib.xmgn_comm_destroy(self.handle)
             self.handle = None
+
+
+def scatter_rows(src, idx, dst, stream=None):
+    """dst[idx[i]] = src[i] (rows; src/dst CUDA float32 2-D, idx CUDA int64)."""
+    import torch
+    n, W = src.shape
+    if idx.dtype != torch.int64 or not idx.is_cuda or not idx.is_contiguous() or idx.numel() < n:
+        raise TypeError("scatter_rows: idx must be a contiguous CUDA int64 tensor of >= n entries")
+    if dst.dim() != 2 or dst.shape[1] != W:
+        raise ValueError(f"scatter_rows: dst shape {tuple(dst.shape)} vs rows of width {W}")
+    _check(_lib.xmgn_scatter_rows(_dev_f32(src, "src", n * W), idx.data_ptr(), n, W,
+                                  _dev_f32(dst, "dst", dst.numel()), _stream(stream)))
 
 
 def launch_count():

@@ -90,6 +90,12 @@ def _two_rank_worker(rank, world, port, q):
     dist.broadcast_object_list(uid, src=0)
     comm = xmgn.Comm(uid[0], world, rank, rank)
     comm.grad_reduce(grad, torch.cuda.current_stream())
+    # inference gather: every rank's owned rows to rank 0, in rank order
+    mine_rows = torch.cat([outs[p] for p in mine]).to(f"cuda:{rank}")
+    oo = b["owned_offsets"]
+    counts = [int(sum(oo[p + 1] - oo[p] for p in bench.assign_parts(4, world, r))) for r in range(world)]
+    recv = torch.empty((sum(counts), H), device=f"cuda:{rank}") if rank == 0 else None
+    comm.gather_rows(mine_rows, recv, counts if rank == 0 else None, torch.cuda.current_stream())
     torch.cuda.synchronize()
     comm.close()
     pr.close()
@@ -97,15 +103,19 @@ def _two_rank_worker(rank, world, port, q):
     pr1 = Processor(b, H, L, device=rank)
     g1 = torch.zeros(pr1.n_params, device=f"cuda:{rank}")
     same = True
+    all_outs = {}
     for p in pr1.parts:
         h0, e0, g = pr1.make_inputs(p)
         o = pr1.forward(p, params, h0, e0).cpu()
+        all_outs[p] = o
         if p in outs:
             same = same and torch.equal(o, outs[p])
         pr1.backward(p, params, g, g1)
     torch.cuda.synchronize()
     rel = float((grad - g1).norm() / g1.norm())
     pr1.close()
+    if rank == 0:   # the gathered rows are every partition's owned rows in partition order
+        same = same and torch.equal(recv.cpu(), torch.cat([all_outs[p] for p in range(4)]))
     q.put((rank, same, rel))
     dist.destroy_process_group()
 
