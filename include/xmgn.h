@@ -179,6 +179,31 @@ void xmgn_comm_destroy(xmgn_comm* comm);
 xmgn_status xmgn_scatter_rows(const float* src, const int64_t* idx, int64_t n, int64_t row_elems, float* dst,
                               void* stream);
 
+/* ------------------------------------------------------------------ optimiser step (NEXT-2)
+ * After gradient aggregation, one update of the flat FP32
+ * parameter vector as PAPER.md:234 (Sec. V-D) trains the model -- "Adam ... with a
+ * cosine annealing learning rate schedule ranging from 1e-3 to 1e-6 ... Gradient
+ * clipping with a threshold of 32" -- read per SPEC.md:373-381:
+ *   g = grad_scale * grad (e.g. 1/(N d), the MSE normalisation);
+ *   g *= min(1, clip / (||g||_2 + 1e-6)), the norm over all n values (global-norm);
+ *   lr(t) = lr_min + (lr_max - lr_min) (1 + cos(pi t / total_steps)) / 2, t = step (0-based,
+ *           clamped to total_steps);
+ *   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;
+ *   p -= lr(t) (m / (1 - b1^(t+1))) / (sqrt(v / (1 - b2^(t+1))) + eps).
+ * params, grad, m, v: device FP32 [n] (m, v zero before step 0, updated in place);
+ * grad is not modified.  norm_out (device, may be NULL) receives ||g||_2 before clipping.
+ * Deterministic (fixed-order reductions).  EINVAL on NULL pointers, step < 0,
+ * betas outside [0, 1), eps <= 0, clip <= 0 or total_steps <= 0.               */
+typedef struct {
+  float lr_max, lr_min;   /* 1e-3, 1e-6 */
+  int64_t total_steps;    /* schedule length T */
+  float beta1, beta2, eps; /* 0.9, 0.999, 1e-8 */
+  float clip;             /* 32 */
+} xmgn_adam_cfg;
+float xmgn_cosine_lr(const xmgn_adam_cfg* cfg, int64_t step);
+xmgn_status xmgn_adam_step(const xmgn_adam_cfg* cfg, int64_t step, float* params, const float* grad, float* m,
+                           float* v, size_t n, float grad_scale, float* norm_out, void* stream);
+
 /* ------------------------------------------------------------------ diagnostics
  * C[M,N] FP32 = A * B^T on tcgen05 with A [M,K] (a_mn_major=0) or [K,M] (=1)
  * and B [N,K] (b_mn_major=0) or [K,N] (=1), BF16 device arrays; K % 64 == 0,

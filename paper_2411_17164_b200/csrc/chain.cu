@@ -5,10 +5,10 @@
 
 namespace xmgn {
 
-template <int H, bool SPLIT, bool BWD, bool F16, bool Z1 = false>
+template <int H, bool SPLIT, bool BWD, bool F16, bool Z1 = false, bool PIPE = false>
 static void chain_launch(const ChainParams& p, int grid, cudaStream_t st) {
   using C = ChainCfg<H, SPLIT>;
-  auto kern = k_chain<H, SPLIT, BWD, F16, Z1>;
+  auto kern = k_chain<H, SPLIT, BWD, F16, Z1, PIPE>;
   // the smem attribute is per device context: one flag per device (set idempotently,
   // so two host threads racing on the same device are harmless)
   static std::atomic<bool> attr[64];
@@ -28,24 +28,40 @@ size_t chain_smem(int H, bool split) {
 }
 
 template <int H, bool F16>
-static void launch_h(bool bwd, const ChainParams& p, int grid, cudaStream_t st) {
+static void launch_h(bool bwd, bool pipe, const ChainParams& p, int grid, cudaStream_t st) {
   bool z1 = false;
   for (int i = 0; i < p.n_steps; ++i) z1 = z1 || (p.steps[i].flags & EF_FROM_IN) != 0;
+  if constexpr (H == 512) {
+    if (pipe && !z1) {
+      if (bwd) chain_launch<H, false, true, F16, false, true>(p, grid, st);
+      else chain_launch<H, false, false, F16, false, true>(p, grid, st);
+      return;
+    }
+  }
   if (bwd && z1) chain_launch<H, false, true, F16, true>(p, grid, st);
   else if (bwd) chain_launch<H, false, true, F16>(p, grid, st);
   else chain_launch<H, false, false, F16>(p, grid, st);
 }
 
-void launch_chain(int H, bool split, bool f16, bool bwd, const ChainParams& p, int grid, cudaStream_t st) {
+bool chain_can_pipe(int H, bool split, const ChainParams& p) {
+  if (H != 512 || split) return false;
+  for (int i = 0; i < p.n_steps; ++i)
+    if (p.steps[i].K != H || (p.steps[i].flags & EF_FROM_IN)) return false;
+  return true;
+}
+
+void launch_chain(int H, bool split, bool f16, bool bwd, const ChainParams& p, int grid, cudaStream_t st,
+                  bool pipe) {
   count_launch();
+  pipe = pipe && chain_can_pipe(H, split, p);
   if (split) {  // FP32 check mode: BF16 hi/lo operands, H = 128
     if (bwd) chain_launch<128, true, true, false>(p, grid, st);
     else chain_launch<128, true, false, false>(p, grid, st);
     return;
   }
-  if (H == 128) { if (f16) launch_h<128, true>(bwd, p, grid, st); else launch_h<128, false>(bwd, p, grid, st); }
-  else if (H == 256) { if (f16) launch_h<256, true>(bwd, p, grid, st); else launch_h<256, false>(bwd, p, grid, st); }
-  else { if (f16) launch_h<512, true>(bwd, p, grid, st); else launch_h<512, false>(bwd, p, grid, st); }
+  if (H == 128) { if (f16) launch_h<128, true>(bwd, false, p, grid, st); else launch_h<128, false>(bwd, false, p, grid, st); }
+  else if (H == 256) { if (f16) launch_h<256, true>(bwd, false, p, grid, st); else launch_h<256, false>(bwd, false, p, grid, st); }
+  else { if (f16) launch_h<512, true>(bwd, pipe, p, grid, st); else launch_h<512, false>(bwd, pipe, p, grid, st); }
 }
 
 }  // namespace xmgn

@@ -332,9 +332,21 @@ namespace xmgn {
 // Z1: backward programs whose first edge step reloads the forward's z_1 checkpoint
 // (a separate instantiation so the regular backward kernel's register allocation is
 // unaffected)
-template <int H, bool SPLIT, bool BWD, bool F16, bool Z1 = false>
+//
+// PIPE (H = 512, 16-bit modes, every step K = H): the step's accumulator is produced as two
+// N-halves (TMEM columns [0,256) and [256,512)) in the order nh = 0 over all K, then nh = 1
+// with K-half 0 before K-half 1.  The epilogue warps of column groups 0-1 own N-half 0 and
+// those of groups 2-3 own N-half 1, each half with its own barriers, so
+//   * half 0's epilogue runs while the MMA computes N-half 1 (it may rewrite ACT half 0 as
+//     soon as N-half 1's K-half-0 MMAs have read it: act_rd[0]);
+//   * the next step's N-half-0 MMAs over K-half 0 start as soon as half 0's epilogue has
+//     written ACT half 0 and drained TMEM half 0, while half 1's epilogue still runs.
+// An A_TMA step stages its A chunk kc straight into ACT block kc (all K = H resident, read by
+// both N-halves).  LayerNorm steps still need both halves' row statistics (row_sum).
+template <int H, bool SPLIT, bool BWD, bool F16, bool Z1 = false, bool PIPE = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THREADS, 1)
     k_chain(const __grid_constant__ ChainParams p) {
+  static_assert(!PIPE || (H == 512 && !SPLIT && !Z1 && EpiShape<SPLIT>::EW == 4), "PIPE: H = 512, 16-bit, 4 groups");
   using C = ChainCfg<H, SPLIT>;
   constexpr int NB = C::NB;
   constexpr int NH = H / NB;           // N-halves per step
@@ -358,7 +370,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
   uint64_t* act_free = act_full + 1;         // MMA -> producer (no MMA reads ACT any more)
   uint64_t* mma_idle = act_free + 1;         // MMA -> itself (all issued MMAs retired)
   uint64_t* in_full = mma_idle + 1;          // [H/64] epilogue input boxes landed in ACT
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(in_full + H / 64);
+  // PIPE: per N-half barriers
+  uint64_t* acc_full2 = in_full + H / 64;    // [2] MMA -> epilogue half h (TMEM half h ready)
+  uint64_t* acc_empty2 = acc_full2 + 2;      // [2] epilogue half h (both CTAs) -> MMA (TMEM half drained)
+  uint64_t* act_full2 = acc_empty2 + 2;      // [2] epilogue half h (both CTAs) -> MMA (ACT half written)
+  uint64_t* act_rd = act_full2 + 2;          // [2] MMA -> epilogue / producer: ACT half no longer read
+  uint64_t* act_idle = act_rd + 2;           // [2] local epilogue half -> local producer: ACT half idle
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(act_idle + 2);
   float* red = reinterpret_cast<float*>(smem + C::RED_OFF);
   float* prm_base = reinterpret_cast<float*>(smem + C::PRM_OFF);
 
@@ -376,6 +394,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
     mbar_init(act_free, 1);
     mbar_init(mma_idle, 1);
     for (int i = 0; i < H / 64; ++i) mbar_init(&in_full[i], 1);
+    if constexpr (PIPE) {
+      for (int h = 0; h < 2; ++h) {
+        mbar_init(&acc_full2[h], 1);
+        mbar_init(&acc_empty2[h], 2);
+        mbar_init(&act_full2[h], 2);
+        mbar_init(&act_rd[h], 1);
+        mbar_init(&act_idle[h], 1);
+      }
+    }
     fence_barrier_init();
   }
   if (w == 0 && lane_id() == 0)
@@ -391,7 +418,90 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
   // the epilogue warpgroups get the rest
   if (w < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(ES::CTRL_REGS) : "memory");
-  if (w == 0) {
+  if (w == 0 && PIPE) {
+    // ============================ PIPE TMA producer: B in MMA order (nh outer, k inner);
+    // A_TMA chunk kc -> ACT block kc once the previous step is done with that ACT half
+    if (elect_one()) {
+      int bi = 0, g = 0;
+      for (int tile = cid; tile < n_tiles; tile += ncl) {
+        const int row0 = tile * 256 + (int)rank * 128;
+        for (int s = 0; s < p.n_steps; ++s, ++g) {
+          const Step& st = p.steps[s];
+          const bool tma_a = st.a_src == A_TMA;
+          constexpr int NK = H / 64;
+          for (int nh = 0; nh < 2; ++nh) {
+            for (int kc = 0; kc < NK; ++kc) {
+              if (tma_a && nh == 0) {
+                const int kh = kc / (NK / 2);
+                if (g > 0 && kc % (NK / 2) == 0) {
+                  mbar_wait(&act_rd[kh], (g - 1) & 1);     // the previous step's MMAs read it
+                  mbar_wait(&act_idle[kh], (g - 1) & 1);   // the previous step's epilogue used it
+                }
+                if (rank == 0) mbar_expect_tx(&a_full[kc], 2 * C::A_SLOT);
+                const uint32_t fb = mapa_shared(smem_u32(&a_full[kc]), 0);
+                const int k = kc * 64;
+                const int mi = (st.a_map1 >= 0 && k >= st.a_ksplit) ? st.a_map1 : st.a_map0;
+                const int kk = (st.a_map1 >= 0 && k >= st.a_ksplit) ? k - st.a_ksplit : k;
+                tma_load_2d_cg2(act + kc * C::A_SLOT, &p.maps[mi], fb, kk, row0);
+              }
+              const int slot = bi % C::SB;
+              if (bi >= C::SB) mbar_wait(&b_empty[slot], ((bi / C::SB) - 1) & 1);
+              if (rank == 0) mbar_expect_tx(&b_full[slot], 2 * C::B_SLOT);
+              const uint32_t fb = mapa_shared(smem_u32(&b_full[slot]), 0);
+              const int brow = st.b_row0 + nh * NB + (int)rank * C::NBH;
+              tma_load_2d_cg2(bring + slot * C::B_SLOT, &p.maps[st.b_map], fb, kc * 64, brow);
+              ++bi;
+            }
+          }
+        }
+      }
+    }
+  } else if (w == 1 && PIPE) {
+    // ============================ PIPE MMA issuer (leader CTA): per step nh = 0 (all K), then
+    // nh = 1 (K-half 0, commit act_rd[0], K-half 1, commit act_rd[1])
+    if (rank == 0) {
+      constexpr uint32_t idesc = idesc_pair(NB, F16);
+      constexpr int NK = H / 64;
+      int bi = 0, g = 0, na = 0;
+      for (int tile = cid; tile < n_tiles; tile += ncl) {
+        for (int s = 0; s < p.n_steps; ++s, ++g) {
+          const Step& st = p.steps[s];
+          const bool tma_a = st.a_src == A_TMA;
+          for (int nh = 0; nh < 2; ++nh) {
+            if (g > 0) mbar_wait(&acc_empty2[nh], (g - 1) & 1);   // TMEM half nh drained
+            for (int kc = 0; kc < NK; ++kc) {
+              const int kh = kc / (NK / 2);
+              if (nh == 0) {
+                if (tma_a) mbar_wait(&a_full[kc], na & 1);
+                else if (g > 0 && kc % (NK / 2) == 0) mbar_wait(&act_full2[kh], (g - 1) & 1);
+              }
+              tc_fence_after();
+              const uint32_t a_base = smem_u32(act + kc * (128 * 128));
+              const int bslot = bi % C::SB;
+              mbar_wait(&b_full[bslot], (bi / C::SB) & 1);
+              tc_fence_after();
+              const uint32_t b_base = smem_u32(bring + bslot * C::B_SLOT);
+              if (elect_one()) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  uint64_t ad = sdesc_sw128(a_base + k * 32, 16, 1024);
+                  uint64_t bd = sdesc_sw128(b_base + k * 32, 16, 1024);
+                  mma_f16_cg2(tmem + nh * NB, ad, bd, idesc, (kc | k) != 0);
+                }
+                mma_commit_cg2_mc(&b_empty[bslot], 3);
+                if (nh == 1 && kc % (NK / 2) == NK / 2 - 1) mma_commit_cg2_mc(&act_rd[kh], 3);
+              }
+              __syncwarp();
+              ++bi;
+            }
+            if (elect_one()) mma_commit_cg2_mc(&acc_full2[nh], 3);
+            __syncwarp();
+          }
+          if (tma_a) ++na;
+        }
+      }
+    }
+  } else if (w == 0) {
     // ============================ TMA producer (both CTAs: own A rows, own half of B)
     if (elect_one()) {
       int ai = 0, bi = 0, g = 0, naf = 0;  // A / B ring fills, global step, act_free phases
@@ -502,6 +612,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         }
       }
     }
+  } else if (PIPE && (w == 3 || w == 2)) {
+    // ============================ PIPE step hand-off of N-half h (warp 3: h = 0, warp 2: h = 1,
+    // idle after the TMEM allocation): joins that half's end-of-step barrier, then arrives on
+    // the leader's acc_empty2[h] / act_full2[h] and on the local act_idle[h]
+    const int h = w == 3 ? 0 : 1;
+    const uint32_t ae_l = mapa_shared(smem_u32(&acc_empty2[h]), 0);
+    const uint32_t af_l = mapa_shared(smem_u32(&act_full2[h]), 0);
+    for (int tile = cid; tile < n_tiles; tile += ncl) {
+      for (int s = 0; s < p.n_steps; ++s) {
+        named_bar(7 + h, 256 + 32);
+        if (lane_id() == 0) {
+          if (rank == 0) {
+            mbar_arrive(&acc_empty2[h]);
+            mbar_arrive(&act_full2[h]);
+          } else {
+            mbar_arrive_cluster(ae_l);
+            mbar_arrive_cluster(af_l);
+          }
+          mbar_arrive(&act_idle[h]);
+        }
+        __syncwarp();
+      }
+    }
   } else if (w == 3) {
     // ============================ step hand-off: joins the epilogue's end-of-step barrier and
     // arrives on the leader's acc_empty / act_full.  A release at cluster scope waits for
@@ -537,6 +670,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
     const int lane = lane_id();
     const int trow = q * 32 + lane;
     const int cb = eg * HC;              // first column of this thread
+    const int hh = PIPE ? (eg >> 1) : 0; // PIPE: the N-half this warp's columns belong to
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + cb;
     // full-row sum of a per-thread partial, identical bits in every group
     auto row_sum = [&](float x) -> float {
@@ -840,6 +974,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
           // MMA-independent row loads, then calls wait(): stage this step's bias / gamma /
           // beta in shared memory, wait for the accumulator.
           auto wait = [&]() {
+            if constexpr (PIPE) {
+              // this N-half's 256 threads stage its 256 columns of bias / gamma / beta
+              const int et = threadIdx.x - 128 - 256 * hh;
+              for (int i = et; i < 3 * 256; i += 256) {
+                const int vec = i >> 8, c = 256 * hh + (i & 255);
+                const float* srcv = vec == 0 ? st.bias : (vec == 1 ? st.gamma : st.beta);
+                prm[vec * H + c] = srcv ? __ldg(srcv + c) : 0.f;
+              }
+              named_bar(5 + hh, 256);
+              mbar_wait(&acc_full2[hh], g & 1);
+              tc_fence_after();
+              mbar_wait(&act_rd[hh], g & 1);   // this step's MMAs no longer read ACT half hh
+            } else {
             const int et = threadIdx.x - 128;
             for (int i = et; i < 3 * H; i += NEPI) {
               const float* srcv = i < H ? st.bias : (i < 2 * H ? st.gamma : st.beta);
@@ -853,11 +1000,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
               named_bar(13, NEPI);
               st_pending = false;
             }
+            }
             if (st.gsrc_map >= 0) {
               // P[src] rows of this warp's 32 tile rows, this column group's boxes: lane j
               // issues box first + j for each group of 4 rows (src ids by shuffle)
-              if (threadIdx.x == 128)
-                for (int b = 0; b < H / 64; ++b) mbar_expect_tx(&in_full[b], 128 * 128);
+              if (threadIdx.x == (PIPE ? 128 + 256 * hh : 128))
+                for (int b = (PIPE ? 4 * hh : 0); b < (PIPE ? 4 * hh + 4 : H / 64); ++b)
+                  mbar_expect_tx(&in_full[b], 128 * 128);
               const bool owner = (cb & 63) == 0;                  // narrow groups share a box
               const int first = cb >> 6, nb = HC >= 64 ? HC / 64 : 1;
 #pragma unroll 1
@@ -871,14 +1020,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
                 }
               }
             }
-            if (st.in_map >= 0 && threadIdx.x == 128) {
+            if (st.in_map >= 0 && threadIdx.x == (PIPE ? 128 + 256 * hh : 128)) {
               // the step's MMAs have read ACT: bulk-load the row input over it, in the order
-              // the column groups consume the 64-column boxes
+              // the column groups consume the 64-column boxes (PIPE: this half's groups only)
               const int row0 = tile * 256 + (int)rank * 128;
               constexpr int BPG = HC >= 64 ? HC / 64 : 1;          // boxes per column group
               constexpr int NG = HC >= 64 ? EW : H / 64;
+              const int g0 = PIPE ? 2 * hh : 0, g1 = PIPE ? 2 * hh + 2 : NG;
               for (int j = 0; j < BPG; ++j)
-                for (int gi = 0; gi < NG; ++gi) {
+                for (int gi = g0; gi < g1; ++gi) {
                   const int b = gi * BPG + j;
                   mbar_expect_tx(&in_full[b], 128 * 128);
                   tma_load_2d(act + b * (128 * 128), &p.maps[st.in_map], &in_full[b], b * 64, row0);
@@ -938,9 +1088,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
             st_pending = true;
           }
           // the next step refills the A ring (aliases ACT): drain before arriving
+          // (PIPE: always -- ACT half hh is handed back at the end of every step)
           {
             const Step& nx = p.steps[s + 1 < p.n_steps ? s + 1 : 0];
-            if (st_pending && nx.a_src == A_TMA && (nx.ctl & CTL_NEED_ACT_FREE)) {
+            if (st_pending && (PIPE || (nx.a_src == A_TMA && (nx.ctl & CTL_NEED_ACT_FREE)))) {
               if (issuer) bulk_wait_read0();
               st_pending = false;
             }
@@ -949,8 +1100,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         tc_fence_before();
         if (wrote_act) fence_proxy_async_smem();
         __syncwarp();
-        // warp 3 arrives on the leader's barriers once every epilogue warp is here
-        named_bar(8, NEPI + 32);
+        // warp 3 (PIPE: warp 3 / 2 for N-half 0 / 1) arrives on the leader's barriers once
+        // every epilogue warp (of the half) is here
+        if constexpr (PIPE) named_bar(7 + hh, 256 + 32);
+        else named_bar(8, NEPI + 32);
       }
     }
   }

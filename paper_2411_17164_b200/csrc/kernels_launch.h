@@ -46,7 +46,11 @@ struct ProfScope {
   cudaEvent_t e0 = nullptr;
 };
 // chain.cu
-void launch_chain(int H, bool split, bool f16, bool bwd, const ChainParams& p, int grid, cudaStream_t st);
+// pipe: use the N-half-pipelined kernel (k_chain PIPE) when the program allows it (H = 512,
+// 16-bit, every step K = H)
+void launch_chain(int H, bool split, bool f16, bool bwd, const ChainParams& p, int grid, cudaStream_t st,
+                  bool pipe = true);
+bool chain_can_pipe(int H, bool split, const ChainParams& p);
 size_t chain_smem(int H, bool split);
 
 }  // namespace xmgn

@@ -69,6 +69,7 @@ struct xmgn_workspace {
   float* d_scale = nullptr;        // {S, 1/S}: the backward's power-of-two loss scale
   int last_fwd = -1;
   bool infer = false;   // inference workspace: forward only, per-layer buffers ping-ponged
+  bool pipe = true;     // N-half-pipelined chain kernel where a program allows it (XMGN_PIPE=0: off)
   // checkpoint slot of layer l's tensors (training: one per layer; inference: ping-pong)
   long long ck(int l) const { return infer ? (l & 1) : l; }
 };
@@ -243,7 +244,7 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
     XMGN_CUDA(cudaMemsetAsync(ws->colsum, 0, (size_t)grid * 4 * NV_MAX * ws->H * sizeof(float), st), "colsum zero");
   {
     ProfScope ps(name, st);
-    launch_chain(ws->H, ws->split, ws->f16, bwd, p, grid, st);
+    launch_chain(ws->H, ws->split, ws->f16, bwd, p, grid, st, ws->pipe);
   }
   XMGN_CUDA(cudaGetLastError(), "chain kernel launch");
 }
@@ -357,6 +358,7 @@ static xmgn_status workspace_create(const xmgn_graph* g, const xmgn_model_cfg* c
       ws->g = g;
       ws->cfg = *cfg;
       ws->infer = infer;
+      { const char* pe = getenv("XMGN_PIPE"); ws->pipe = !(pe && atoi(pe) == 0); }
       ws->dev = g->device;
       ws->H = H; ws->L = L; ws->m = m;
       ws->split = cfg->precision == XMGN_PREC_FP32_CHECK;

@@ -46,6 +46,12 @@ class ModelCfg(ctypes.Structure):
                 ("precision", ctypes.c_int32), ("ln_eps", ctypes.c_float)]
 
 
+class AdamCfg(ctypes.Structure):
+    _fields_ = [("lr_max", ctypes.c_float), ("lr_min", ctypes.c_float), ("total_steps", _i64),
+                ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float),
+                ("clip", ctypes.c_float)]
+
+
 def _sig(name, res, args):
     f = getattr(_lib, name)
     f.restype, f.argtypes = res, args
@@ -72,6 +78,8 @@ _sig("xmgn_grad_reduce", _i32, [_vp, _vp, _sz, _vp])
 _sig("xmgn_comm_destroy", None, [_vp])
 _sig("xmgn_gather_rows", _i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp])
 _sig("xmgn_scatter_rows", _i32, [_vp, _vp, _i64, _i64, _vp, _vp])
+_sig("xmgn_cosine_lr", ctypes.c_float, [ctypes.POINTER(AdamCfg), _i64])
+_sig("xmgn_adam_step", _i32, [ctypes.POINTER(AdamCfg), _i64, _vp, _vp, _vp, _vp, _sz, ctypes.c_float, _vp, _vp])
 _sig("xmgn_selftest_gemm", _i32, [_i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp])
 _sig("xmgn_launch_count", ctypes.c_longlong, [])
 _sig("xmgn_profile_enable", _i32, [_i32])
@@ -84,7 +92,7 @@ EXPORTS = ["xmgn_last_error", "xmgn_version", "xmgn_load_graph", "xmgn_part_info
            "xmgn_workspace_free", "xmgn_processor_fwd", "xmgn_processor_bwd", "xmgn_check_finite",
            "xmgn_comm_unique_id", "xmgn_comm_init", "xmgn_grad_reduce", "xmgn_comm_destroy", "xmgn_gather_rows",
            "xmgn_scatter_rows",
-           "xmgn_selftest_gemm", "xmgn_launch_count", "xmgn_profile_enable", "xmgn_profile_collect"]
+           "xmgn_cosine_lr", "xmgn_adam_step", "xmgn_selftest_gemm", "xmgn_launch_count", "xmgn_profile_enable", "xmgn_profile_collect"]
 
 
 def _check(status):
@@ -294,6 +302,30 @@ def scatter_rows(src, idx, dst, stream=None):
         raise ValueError(f"scatter_rows: dst shape {tuple(dst.shape)} vs rows of width {W}")
     _check(_lib.xmgn_scatter_rows(_dev_f32(src, "src", n * W), idx.data_ptr(), n, W,
                                   _dev_f32(dst, "dst", dst.numel()), _stream(stream)))
+
+
+class Adam:
+    """xmgn_adam_step: global-norm clip + Adam + cosine LR on a flat FP32 parameter vector
+    (PAPER.md:234 defaults: 1e-3 -> 1e-6, clip 32, betas 0.9 / 0.999, eps 1e-8)."""
+
+    def __init__(self, n, total_steps, device=0, lr_max=1e-3, lr_min=1e-6, beta1=0.9, beta2=0.999, eps=1e-8,
+                 clip=32.0):
+        import torch
+        self.cfg = AdamCfg(lr_max, lr_min, int(total_steps), beta1, beta2, eps, clip)
+        self.m = torch.zeros(n, device=f"cuda:{device}")
+        self.v = torch.zeros(n, device=f"cuda:{device}")
+        self.norm = torch.zeros(1, device=f"cuda:{device}")
+        self.t = 0
+
+    def lr(self, step=None):
+        return float(_lib.xmgn_cosine_lr(ctypes.byref(self.cfg), self.t if step is None else int(step)))
+
+    def step(self, params, grad, grad_scale=1.0, stream=None):
+        n = params.numel()
+        _check(_lib.xmgn_adam_step(ctypes.byref(self.cfg), self.t, _dev_f32(params, "params", n),
+                                   _dev_f32(grad, "grad", n), _dev_f32(self.m, "m", n), _dev_f32(self.v, "v", n), n,
+                                   float(grad_scale), self.norm.data_ptr(), _stream(stream)))
+        self.t += 1
 
 
 def launch_count():
