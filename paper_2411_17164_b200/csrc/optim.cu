@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <cmath>
 #include "kernels_launch.h"
+#include "xmgn_internal.h"
 
 namespace xmgn {
 
