@@ -101,6 +101,13 @@ struct Step {
   int st_map;
 };
 
+// does the epilogue of step st read or write the ACT tile (outputs, TMA-staged inputs, stores)?
+__host__ __device__ inline bool step_uses_act(const Step& st) {
+  const bool writes = st.epi == EPI_SILU || st.epi == EPI_LN_BWD || st.epi == EPI_DSILU ||
+                      (st.epi == EPI_LN_FWD && (st.flags & EF_WRITE_ACT));
+  return writes || st.in_map >= 0 || st.gsrc_map >= 0 || st.st_map >= 0;
+}
+
 constexpr int MAX_STEPS = 8;
 constexpr int MAX_MAPS = 24;
 constexpr int NV_MAX = 5;  // column-sum vectors per kernel
@@ -435,7 +442,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
                 const int kh = kc / (NK / 2);
                 if (g > 0 && kc % (NK / 2) == 0) {
                   mbar_wait(&act_rd[kh], (g - 1) & 1);     // the previous step's MMAs read it
-                  mbar_wait(&act_idle[kh], (g - 1) & 1);   // the previous step's epilogue used it
+                  // the previous step's epilogue used it (skipped when that epilogue never touches
+                  // ACT: the A loads then overlap it)
+                  const Step& pv = p.steps[s > 0 ? s - 1 : p.n_steps - 1];
+                  if (step_uses_act(pv)) mbar_wait(&act_idle[kh], (g - 1) & 1);
                 }
                 if (rank == 0) mbar_expect_tx(&a_full[kc], 2 * C::A_SLOT);
                 const uint32_t fb = mapa_shared(smem_u32(&a_full[kc]), 0);
@@ -623,6 +633,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
       for (int s = 0; s < p.n_steps; ++s) {
         named_bar(7 + h, 256 + 32);
         if (lane_id() == 0) {
+          // act_idle first: once the MMA has seen this step's acc_empty, act_idle has completed
+          // this step's phase too, so the producer's parity waits never see it two phases behind
+          mbar_arrive(&act_idle[h]);
           if (rank == 0) {
             mbar_arrive(&acc_empty2[h]);
             mbar_arrive(&act_full2[h]);
@@ -630,7 +643,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
             mbar_arrive_cluster(ae_l);
             mbar_arrive_cluster(af_l);
           }
-          mbar_arrive(&act_idle[h]);
         }
         __syncwarp();
       }
