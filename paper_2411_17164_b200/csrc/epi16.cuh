@@ -177,6 +177,23 @@ __device__ __forceinline__ void in16(const Epi& e, int c0, float* v) {
   lds_tile16<F16>(e.act, e.trow, c0, v);
 }
 
+// Deferred form for the per-chunk dgamma sums: the warp sum of chunk cc is kept in
+// acc[cc] (lanes 0-15 hold column c0 + lane) and colsum16_flush issues all NC read-modify-
+// writes back to back (one exposed global latency per step instead of NC).
+template <int NC>
+__device__ __forceinline__ void colsum16_flush(const Epi& e, int vec, const float* acc) {
+  constexpr int HT = NC * 16 * 4;   // H (4 column groups of NC x 16)
+  const int lane = lane_id();
+  if (lane < 16) {
+    float* d = e.colsum + (size_t)vec * HT + e.cb + lane;
+    float old[NC];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) old[cc] = d[cc * 16];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) d[cc * 16] = old[cc] + acc[cc];
+  }
+}
+
 template <int H>
 __device__ __forceinline__ void colsum16_add(const Epi& e, int vec, int c0, float* vals) {
   const float cs = warp_colsum16(vals);
@@ -416,6 +433,7 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
   float mean, rstd;
   ln_stats16<H, NC>(e, e.eps, row_sum, mean, rstd);
   float s1 = 0.f, s2 = 0.f;
+  float dg[NC];   // deferred dgamma warp sums (colsum16_flush)
   uint32_t ta[16];
   tmem_ld16_async(e.tl, ta);
   auto passA = [&](int cc, uint32_t* gq, uint32_t* aq) {
@@ -445,18 +463,19 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
       s2 += dxh * xh[i];
       gm[i] = e.valid ? dy[i] * xh[i] : 0.f;       // dgamma terms
     }
-    colsum16_add<H>(e, 0, c0, gm);
+    dg[cc] = warp_colsum16(gm);
     if (csall) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) xh[i] = e.valid ? dy[i] : 0.f;
       colsum16_add<H>(e, 1, c0, xh);                 // dbeta
     }
   };
-#pragma unroll 1
+#pragma unroll
   for (int cc = 0; cc < NC; cc += 2) {
     passA(cc, g0, a0);
     passA(cc + 1, g1, a1);
   }
+  colsum16_flush<NC>(e, 0, dg);
   s1 = row_sum(s1) * (1.0f / H);
   s2 = row_sum(s2) * (1.0f / H);
   tmem_ld16_async(e.tl, ta);

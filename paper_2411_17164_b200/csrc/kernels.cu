@@ -261,6 +261,74 @@ __global__ void __launch_bounds__(256) k_segsum(const int* __restrict__ off, con
   }
 }
 
+// 16-bit fast path of the same sums: two warps per node (t = 2i: the out-edge half through rev,
+// t = 2i + 1: the in-edge half), the segment's edge indices fetched 32 at a time with one
+// coalesced load and broadcast by shuffles, then batches of B rows in flight.  Each half row is
+// summed in CSR order exactly as k_segsum does, so the result is bitwise the same.
+template <int H, bool F16>
+__global__ void __launch_bounds__(256, 4) k_segsum16(const int* __restrict__ off, const int* __restrict__ rev,
+                                                  const __nv_bfloat16* __restrict__ dz, __nv_bfloat16* __restrict__ D,
+                                                  int n, int e_act) {
+  constexpr int V = H / 8 / 32;            // 16-byte chunks per lane of one H-wide half (H >= 256)
+  static_assert(V >= 1, "k_segsum16: H >= 256");
+  constexpr int B = 4;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < 2 * n; t += nw) {
+    const int i = t >> 1, part = t & 1;
+    const int k0 = off[i], k1 = off[i + 1];
+    float acc[V][8];
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[v][q] = 0.f;
+    for (int base = k0; base < k1; base += 32) {
+      const int cnt = min(32, k1 - base);
+      int myk = e_act;                    // >= e_act: contributes nothing
+      if (lane < cnt) myk = part ? base + lane : rev[base + lane];
+      int j = 0;
+      for (; j + B <= cnt; j += B) {
+        uint4 u[B][V];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          const int kk = __shfl_sync(0xffffffffu, myk, j + b);
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            u[b][v] = kk < e_act ? __ldg(reinterpret_cast<const uint4*>(dz + (size_t)kk * H) + lane + 32 * v)
+                                 : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            float x[8];
+            unpack8<F16>(u[b][v], x);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[v][q] += x[q];
+          }
+      }
+      for (; j < cnt; ++j) {
+        const int kk = __shfl_sync(0xffffffffu, myk, j);
+        if (kk >= e_act) continue;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          float x[8];
+          unpack8<F16>(__ldg(reinterpret_cast<const uint4*>(dz + (size_t)kk * H) + lane + 32 * v), x);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[v][q] += x[q];
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) split2<F16, false>(acc[v][2 * q], acc[v][2 * q + 1], hi[q], lo[q]);
+      reinterpret_cast<uint4*>(D + (size_t)i * 2 * H + part * H)[lane + 32 * v] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- weight gradient dW = A^T dZ (split-K)
 // D[m = input feature][n = output feature] += sum_rows A[row][m] dZ[row][n].
 // Both operands are read straight from their row-major BF16 tensors as
@@ -523,6 +591,12 @@ void launch_aggregate32(int H, const int* off, const float* e, __nv_bfloat16* a,
 template <bool F16>
 static void seg_t(int H, const int* off, const int* rev, const __nv_bfloat16* dz, long long dz_lo, __nv_bfloat16* D,
                   long long d_lo, int n, int e_act, cudaStream_t st) {
+  if (!dz_lo && !d_lo && H >= 256) {
+    const int blocks16 = std::min((2 * n + 7) / 8, 148 * 16);
+    if (H == 256) k_segsum16<256, F16><<<blocks16, 256, 0, st>>>(off, rev, dz, D, n, e_act);
+    else k_segsum16<512, F16><<<blocks16, 256, 0, st>>>(off, rev, dz, D, n, e_act);
+    return;
+  }
   int blocks = std::min((n + 7) / 8, 148 * 16);
   if (H == 128) k_segsum<128, F16><<<blocks, 256, 0, st>>>(off, rev, dz, dz_lo, D, d_lo, n, e_act);
   else if (H == 256) k_segsum<256, F16><<<blocks, 256, 0, st>>>(off, rev, dz, dz_lo, D, d_lo, n, e_act);

@@ -243,11 +243,6 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
   if (bwd)
     XMGN_CUDA(cudaMemsetAsync(ws->colsum, 0, (size_t)grid * 4 * NV_MAX * ws->H * sizeof(float), st), "colsum zero");
   const bool pipe = ws->pipe && chain_can_pipe(ws->H, ws->split, p);
-  if (pipe && p.steps[n - 1].in_map >= 0 && p.steps[0].a_src == A_TMA) {
-    // PIPE: the last step's epilogue reads its row input with plain loads instead of staging it
-    // in ACT, so the next tile's A operand can stream into ACT while that epilogue runs
-    p.steps[n - 1].in_map = -1;
-  }
   {
     ProfScope ps(name, st);
     launch_chain(ws->H, ws->split, ws->f16, bwd, p, grid, st, pipe);
