@@ -14,6 +14,11 @@
 #pragma once
 #include "tc.cuh"
 
+// dgamma column sums of the LN backward: deferred read-modify-writes (1) or one per chunk (0)
+#ifndef XMGN_DEFER_DGAMMA
+#define XMGN_DEFER_DGAMMA 1
+#endif
+
 namespace xmgn {
 
 // ---- 16-column helpers
@@ -463,19 +468,32 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
       s2 += dxh * xh[i];
       gm[i] = e.valid ? dy[i] * xh[i] : 0.f;       // dgamma terms
     }
+#if XMGN_DEFER_DGAMMA
     dg[cc] = warp_colsum16(gm);
+#else
+    colsum16_add<H>(e, 0, c0, gm);
+#endif
     if (csall) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) xh[i] = e.valid ? dy[i] : 0.f;
       colsum16_add<H>(e, 1, c0, xh);                 // dbeta
     }
   };
+#if XMGN_DEFER_DGAMMA
 #pragma unroll
   for (int cc = 0; cc < NC; cc += 2) {
     passA(cc, g0, a0);
     passA(cc + 1, g1, a1);
   }
   colsum16_flush<NC>(e, 0, dg);
+#else
+  (void)dg;
+#pragma unroll 1
+  for (int cc = 0; cc < NC; cc += 2) {
+    passA(cc, g0, a0);
+    passA(cc + 1, g1, a1);
+  }
+#endif
   s1 = row_sum(s1) * (1.0f / H);
   s2 = row_sum(s2) * (1.0f / H);
   tmem_ld16_async(e.tl, ta);
