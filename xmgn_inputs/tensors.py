@@ -131,3 +131,51 @@ def params(H, L, m=2, device="cpu"):
             v = sym_uniform(SEED_PARAMS, tid, rows, ncol, 1.0 / math.sqrt(fan), device)
         p[off:off + v.numel()] = v.reshape(-1)
     return p
+
+
+# ---------------------------------------------------------------- model inputs (NEXT-1)
+SEED_TARGETS, SEED_IO = 5, 6
+F_NODE, F_EDGE, D_OUT = 24, 4, 4   # PAPER.md:234 (24 inputs), :161 (4 edge features), :217 (p, tau)
+
+
+def io_param_layout(H, m=2, fn=F_NODE, fe=F_EDGE, d=D_OUT):
+    """(name, block, slot, offset, shape, fan_in) of the encoder / decoder parameters in
+    the C-ABI order (include/xmgn.h): node encoder, edge encoder (W1, b1, ..., gamma,
+    beta), decoder (W1, b1, ..., W_{m+1} [H x d], b_{m+1} [d])."""
+    out, off = [], 0
+    for blk, fin in ((0, fn), (1, fe)):
+        slot = 0
+        for j in range(m + 1):
+            kin = fin if j == 0 else H
+            out.append((f"W{j+1}", blk, slot, off, (kin, H), kin)); off += kin * H; slot += 1
+            out.append((f"b{j+1}", blk, slot, off, (H,), kin)); off += H; slot += 1
+        out.append(("gamma", blk, slot, off, (H,), H)); off += H; slot += 1
+        out.append(("beta", blk, slot, off, (H,), H)); off += H; slot += 1
+    slot = 0
+    for j in range(m + 1):
+        nout = d if j == m else H
+        out.append((f"W{j+1}", 2, slot, off, (H, nout), H)); off += H * nout; slot += 1
+        out.append((f"b{j+1}", 2, slot, off, (nout,), H)); off += nout; slot += 1
+    return out, off
+
+
+def io_params(H, m=2, device="cpu"):
+    lay, n = io_param_layout(H, m)
+    p = torch.empty(n, dtype=torch.float32, device=device)
+    for name, blk, slot, off, shape, fan in lay:
+        tid = blk * 16 + slot
+        rows = torch.arange(shape[0], device=device)
+        ncol = shape[1] if len(shape) == 2 else 1
+        if name == "gamma":
+            v = (1.0 + sym_uniform(SEED_IO, tid, rows, ncol, 0.1 * SQRT3, device)).to(torch.bfloat16).to(torch.float32)
+        elif name == "beta":
+            v = sym_uniform(SEED_IO, tid, rows, ncol, 0.1 * SQRT3, device)
+        else:
+            v = sym_uniform(SEED_IO, tid, rows, ncol, 1.0 / math.sqrt(fan), device)
+        p[off:off + v.numel()] = v.reshape(-1)
+    return p
+
+
+def targets(gids, device="cpu"):
+    """Synthetic z-scored targets (p, tau_x, tau_y, tau_z) ~ U(+-sqrt3) per node."""
+    return sym_uniform(SEED_TARGETS, 0, gids, D_OUT, SQRT3, device)
