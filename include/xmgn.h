@@ -157,6 +157,41 @@ xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const float* params
  * finite.                                                  */
 xmgn_status xmgn_check_finite(const float* dev, size_t n, void* stream);
 
+/* ------------------------------------------------------------------ the model around the processor (NEXT-1)
+ * encoders -> processor -> decoder -> owned-row MSE, the paper's full model:
+ *  - node inputs, 24 per point ("24 input features, including Fourier features
+ *    with 3 different frequencies (i.e., 2pi, 4pi, 8pi)"): [x(3), n(3), then for f in (2pi, 4pi,
+ *    8pi), coordinate c in (x, y, z): sin(f c), cos(f c)] (SPEC.md:134-141 column order);
+ *  - edge inputs, 4 per edge: (x_src - x_dst, ||x_src - x_dst||);
+ *  - both z-scored with the caller's per-variable global mean / std:
+ *    stats = device FP32 [56] = mean of the 24 node and 4 edge inputs, then their std (std > 0);
+ *  - encoders: MLP (m SiLU hidden layers, linear output) + LayerNorm, no residual -> h^0, e^0;
+ *  - decoder: MLP to 4 outputs (p, tau_x, tau_y, tau_z), no LayerNorm;
+ *  - loss: sum over the OWNED rows of (y - t)^2 / (4 n_global) ("Halo nodes are
+ *    filtered out before the loss computation"; PAPER.md:234 MSE): summed over all partitions it is
+ *    the full graph's MSE, and so are the gradients.
+ * IO parameters: one flat FP32 vector, node encoder [W_0 (24 x H), b_0, W_j (H x H), b_j for
+ * j = 1..m, gamma, beta], edge encoder [W_0 (4 x H), b_0, ..., gamma, beta], decoder [W_0, b_0,
+ * ..., W_{m-1}, b_{m-1} (H x H), W_m (H x 4), b_m (4)], y = x W + b, W stored [in, out].
+ * 16-bit operand modes only (the FP32 check mode is EUNSUPPORTED).                         */
+size_t xmgn_io_param_count(const xmgn_model_cfg* cfg);
+/* Forward of partition `part`: pos, nrm = device FP32 [n_local, 3] in local order (positions,
+ * unit normals); targets = device FP32 [n_owned, 4] z-scored targets of the owned rows or NULL;
+ * n_global = node count of the whole graph (the MSE's normalisation).  pred (device FP32
+ * [n_owned, 4]) receives the owned rows' predictions (halo predictions are discarded,
+ * PAPER.md:197); with targets, *loss (device FP32) += this partition's loss.  Also valid on an
+ * inference workspace.  The encoder/decoder buffers (~ (N_max + E_max) x 128 B + 13 x owned x H B)
+ * are allocated on the first call.  EINVAL: NULL pointers, targets without loss or n_global <
+ * n_owned.                                                                                     */
+xmgn_status xmgn_model_fwd(xmgn_workspace* ws, int part, const float* params, const float* io_params,
+                           const float* pos, const float* nrm, const float* stats, const float* targets,
+                           int64_t n_global, float* pred, float* loss, void* stream);
+/* Backward of the last xmgn_model_fwd WITH targets on this workspace (else ESTATE): grad_params
+ * [param_count] and grad_io [io_param_count] are ACCUMULATED (+=), so partitions sum in call
+ * order.                                                                       */
+xmgn_status xmgn_model_bwd(xmgn_workspace* ws, int part, const float* params, const float* io_params,
+                           float* grad_params, float* grad_io, void* stream);
+
 /* ------------------------------------------------------------------ gradient aggregation
  * One NCCL communicator per process/GPU (one process per GPU).  The unique id
  * is created on rank 0 and broadcast by the caller (e.g. torch.distributed).

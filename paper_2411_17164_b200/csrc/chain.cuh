@@ -53,7 +53,10 @@ enum : int {
                        // LN_BWD writes dY = g16 (+ ga16[dst]) back into g16; ADD does g16 += acc
   EF_DISCARD = 2048,   // EPI_DSILU: this is the last read of S' -- drop its L2 lines afterwards
   EF_STORE_Z = 8192,   // EPI_SILU (16-bit modes): round z to 16 bits, store it to scr_z, SiLU the rounded z
-  EF_FROM_IN = 16384   // EPI_SILU (16-bit modes): z is the TMA row input in ACT (a K = 0 step, no MMA)
+  EF_FROM_IN = 16384,  // EPI_SILU (16-bit modes): z is the TMA row input in ACT (a K = 0 step, no MMA)
+  EF_NO_RES = 32768,   // EPI_LN_FWD (16-bit modes): y = LN(z), no residual (the encoders, NEXT-1)
+  EF_NO_ACT = 65536,   // EPI_DSILU (16-bit modes): dZ leaves by row stores only, ACT untouched (last step)
+  EF_NO_GA = 131072    // EPI_LN_BWD + EF_G16: dY = G rows only (no G_a[dst] term, no write-back)
 };
 
 enum : int {
@@ -102,10 +105,13 @@ struct Step {
 };
 
 // does the epilogue of step st read or write the ACT tile (outputs, TMA-staged inputs, stores)?
+// does the epilogue of step st write the ACT tile (the next step's A operand)?
+__host__ __device__ inline bool step_writes_act(const Step& st) {
+  return st.epi == EPI_SILU || st.epi == EPI_LN_BWD || (st.epi == EPI_DSILU && !(st.flags & EF_NO_ACT)) ||
+         (st.epi == EPI_LN_FWD && (st.flags & EF_WRITE_ACT));
+}
 __host__ __device__ inline bool step_uses_act(const Step& st) {
-  const bool writes = st.epi == EPI_SILU || st.epi == EPI_LN_BWD || st.epi == EPI_DSILU ||
-                      (st.epi == EPI_LN_FWD && (st.flags & EF_WRITE_ACT));
-  return writes || st.in_map >= 0 || st.gsrc_map >= 0 || st.st_map >= 0;
+  return step_writes_act(st) || st.in_map >= 0 || st.gsrc_map >= 0 || st.st_map >= 0;
 }
 
 constexpr int MAX_STEPS = 8;
@@ -658,8 +664,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
     for (int tile = cid; tile < n_tiles; tile += ncl) {
       for (int s = 0; s < p.n_steps; ++s, ++g) {
         const Step& st = p.steps[s];
-        const bool wa = st.epi == EPI_SILU || st.epi == EPI_LN_BWD || st.epi == EPI_DSILU ||
-                        (st.epi == EPI_LN_FWD && (st.flags & EF_WRITE_ACT));
+        const bool wa = step_writes_act(st);
         named_bar(8, NEPI + 32);
         if (lane_id() == 0) {
           if (rank == 0) {          // the leader's own barriers: CTA-scope release suffices
@@ -1077,7 +1082,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
               wrote_act = true;
             } else if (op == EPI_DSILU) {
               op_dsilu<H, NC16, F16>(e, st, wait);
-              wrote_act = true;
+              wrote_act = !(st.flags & EF_NO_ACT);
             }
           }
           // rows this step wrote with ordinary stores that a later step of this kernel reads

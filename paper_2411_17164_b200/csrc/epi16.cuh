@@ -360,7 +360,7 @@ __device__ __forceinline__ void op_ln_fwd(const Epi& e, const Step& st, Wait wai
   constexpr int W = IN32 ? 16 : 8;
   const bool w32 = e.valid && (st.flags & EF_STORE_F32) != 0;
   const bool w16 = e.valid && (st.flags & EF_STORE_BF) != 0, wact = (st.flags & EF_WRITE_ACT) != 0;
-  const bool has_res = e.valid;
+  const bool has_res = e.valid && !(st.flags & EF_NO_RES);
   const __nv_bfloat16* rp16 = st.res16 + (size_t)e.r * H + e.cb;
   const float* rp32 = st.f_in + (size_t)e.r * st.ld_in + e.cb;
   float* op32 = st.f_out + (size_t)e.r * st.ld_out + e.cb;
@@ -425,6 +425,7 @@ template <int H, int NC, bool F16, class Wait, class RowSum>
 __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait wait, RowSum row_sum) {
   const bool csall = (st.flags & EF_COLSUM_ALL) != 0;
   const bool has_g = e.valid && e.r < st.valid_in;
+  const bool ga = e.valid && !(st.flags & EF_NO_GA);   // G_a[dst] term + G_e' write-back
   __nv_bfloat16* gp16 = st.g16 + (size_t)e.r * H + e.cb;
   const __nv_bfloat16* ap16 = st.ga16 + (size_t)e.dst * H + e.cb;
   __nv_bfloat16* zp = st.scr_z + (size_t)e.r * H + e.cb;
@@ -433,7 +434,7 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
   for (int i = 0; i < 8; ++i) g0[i] = g1[i] = a0[i] = a1[i] = 0u;
   const bool tin = st.in_map >= 0;   // G_e rows arrive in ACT by TMA (rows >= valid_in read zero)
   if (has_g && !tin) { ld16(gp16, g0); ld16(gp16 + 16, g1); }
-  if (e.valid) { ld16(ap16, a0); ld16(ap16 + 16, a1); }
+  if (ga) { ld16(ap16, a0); ld16(ap16 + 16, a1); }
   wait();
   float mean, rstd;
   ln_stats16<H, NC>(e, e.eps, row_sum, mean, rstd);
@@ -446,13 +447,13 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
     float dy[16], xh[16];
     if (tin) in16<F16>(e, c0, dy);
     else cvt16<F16>(gq, dy);
-    add16<F16>(aq, dy);
+    if (ga) add16<F16>(aq, dy);
     if (cc + 2 < NC) {
       if (has_g && !tin) ld16(gp16 + (cc + 2) * 16, gq);
-      if (e.valid) ld16(ap16 + (cc + 2) * 16, aq);
+      if (ga) ld16(ap16 + (cc + 2) * 16, aq);
     }
     round16<F16>(dy);                                // as stored (G_e')
-    if (e.valid) st16<F16>(gp16 + cc * 16, dy);
+    if (ga) st16<F16>(gp16 + cc * 16, dy);
     sts_tile16<F16>(e.act, e.trow, c0, dy);          // stash for pass B
     lds16(e.sb + cc * 16, xh);
     tmem_wait16(ta);
@@ -600,6 +601,7 @@ __device__ __forceinline__ void op_ln_bwd32(const Epi& e, const Step& st, Wait w
 template <int H, int NC, bool F16, class Wait>
 __device__ __forceinline__ void op_dsilu(const Epi& e, const Step& st, Wait wait) {
   const bool csall = (st.flags & EF_COLSUM_ALL) != 0;
+  const bool noact = (st.flags & EF_NO_ACT) != 0;   // last step of a program: rows out, ACT untouched
   const __nv_bfloat16* sp = st.scr_s + (size_t)e.r * H + e.cb;
   __nv_bfloat16* zp = st.scr_z + (size_t)e.r * H + e.cb;
   uint32_t q0[8], q1[8];
@@ -620,8 +622,8 @@ __device__ __forceinline__ void op_dsilu(const Epi& e, const Step& st, Wait wait
 #pragma unroll
     for (int i = 0; i < 16; ++i) x[i] *= __uint_as_float(ta[i]);
     if (cc + 1 < NC) tmem_ld16_async(e.tl + (cc + 1) * 16, ta);
-    sts_tile16<F16>(e.act, e.trow, c0, x);
-    if (e.valid && st.st_map < 0) st16<F16>(zp + cc * 16, x);
+    if (!noact) sts_tile16<F16>(e.act, e.trow, c0, x);
+    if (e.valid && (st.st_map < 0 || noact)) st16<F16>(zp + cc * 16, x);
     if (csall) colsum16_add<H>(e, st.vec0, c0, x);
   };
 #pragma unroll 1

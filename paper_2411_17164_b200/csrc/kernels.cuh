@@ -8,6 +8,10 @@
 
 namespace xmgn {
 
+// model inputs / outputs (NEXT-1): 24 node and 4 edge raw inputs, padded to
+// one 64-column operand box; stats = [mean(28) | std(28)]; 4 outputs (p, tau)
+constexpr int IO_F_NODE = 24, IO_F_EDGE = 4, IO_IN_COLS = 64, IO_NSTAT = 28, IO_DOUT = 4;
+
 struct PackJob {            // out[r][c] = bf16(params[src + r*sr + c*sc]), r < rows, c < cols
   __nv_bfloat16* dst;
   long long lo_off;         // lo copy at dst + lo_off (0 = none)

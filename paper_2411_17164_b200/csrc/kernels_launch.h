@@ -35,6 +35,20 @@ void launch_reduce_colsum(const float* part, int nblk, int nv, int H, ColsumDst 
 void launch_scatter_rows(const float* src, const long long* idx, long long n, long long row_elems, float* dst,
                          cudaStream_t st);
 void launch_nonfinite(const float* x, long long n, int* flag, cudaStream_t st);
+// model around the processor (io_kernels.cu, NEXT-1)
+void launch_node_inputs(bool f16, const float* pos, const float* nrm, const float* stats, long long n,
+                        __nv_bfloat16* X, cudaStream_t st);
+void launch_edge_inputs(bool f16, const float* pos, const int* src, const int* dst, const float* stats, long long n,
+                        __nv_bfloat16* X, cudaStream_t st);
+int dec_head_warps(long long n);   // per-warp partials the decoder head writes
+void launch_dec_head(bool f16, int H, const float* zraw, long long n, const float* bm, const float* Wl,
+                     const float* bl, const float* t, float inv_nd, float S, float* pred, double* sse_part,
+                     __nv_bfloat16* dZ, float* wpart, cudaStream_t st);
+void launch_loss_reduce(const double* part, int n, float inv_nd, float* loss, cudaStream_t st);
+int wgrad_thin_blocks(long long rows);
+void launch_wgrad_thin(bool f16, int fn, const __nv_bfloat16* X, const __nv_bfloat16* dZ, long long rows, int H,
+                       float* part, cudaStream_t st);
+void launch_set_scale(float* s, float a, float b, cudaStream_t st);
 // profiling (processor.cu): every kernel launch of the library is counted;
 // when enabled, named launch scopes are bracketed by CUDA events on their stream.
 void count_launch(int n = 1);

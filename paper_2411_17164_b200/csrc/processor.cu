@@ -13,6 +13,7 @@
 // updates destinations of ring <= L-l, a prefix of nodes (n_l) and of edges
 // (E_l); the skipped rows feed only discarded halo outputs.
 #include <cuda_runtime.h>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -68,6 +69,25 @@ struct xmgn_workspace {
   unsigned int* d_amax = nullptr;  // max|g| bits of the current backward's seed
   float* d_scale = nullptr;        // {S, 1/S}: the backward's power-of-two loss scale
   int last_fwd = -1;
+  int gc_last = 0;      // which G_e buffer holds dL/de^0 after the last backward
+  // ---- the model around the processor (NEXT-1), allocated at the first xmgn_model_fwd
+  bool io_ready = false;
+  int64_t Omax = 0;               // largest owned set
+  int S3 = 0;                     // H x H slots of wioH
+  xmgn::BfBuf wio64, wioH;        // encoder W1^T [2][H][64] (zero-padded K); [S3][H][H] (W^T fwd, W dgrad)
+  xmgn::PackJob* d_jobs_io = nullptr;
+  int njobs_io = 0;
+  xmgn::BfBuf Xn, Xe;             // 16-bit z-scored inputs [Nmax][64], [Emax][64]
+  xmgn::BfBuf hL16;               // 16-bit h^L of the owned rows [Omax][H] (the decoder's operand)
+  float* zdec = nullptr;          // FP32 [Omax][H]: A_{m-1} W_{m-1} of the decoder (no bias)
+  xmgn::BfBuf dZdec;              // 16-bit [Omax][H]: S x dL/dz_{m-1} from the head
+  float* gdec = nullptr;          // FP32 [Omax][H]: dL/dh^L (the processor's upstream gradient)
+  double* sse_part = nullptr;     // per-warp SSE partials of the head
+  float* wpart = nullptr;         // per-warp [H*4 + 4] partials of dW_m, db_m
+  float* thin_part = nullptr;     // per-block [24][H] partials of the encoders' dW_1
+  float* d_scale_dec = nullptr;   // {S, 1/S} of the decoder backward
+  int last_model_fwd = -1;        // part of the last xmgn_model_fwd with targets (else -1)
+  int head_warps = 0;
   bool infer = false;   // inference workspace: forward only, per-layer buffers ping-ponged
   bool pipe = true;     // N-half-pipelined chain kernel where a program allows it (XMGN_PIPE=0: off)
   // checkpoint slot of layer l's tensors (training: one per layer; inference: ping-pong)
@@ -192,13 +212,7 @@ struct Prog {
   }
 };
 
-static bool epi_writes_act(const Step& s) {
-  switch (s.epi) {
-    case EPI_SILU: case EPI_LN_BWD: case EPI_DSILU: return true;
-    case EPI_LN_FWD: return (s.flags & EF_WRITE_ACT) != 0;
-    default: return false;
-  }
-}
+static bool epi_writes_act(const Step& s) { return step_writes_act(s); }
 
 // Derive the ACT hand-off controls (chain.cuh) and launch.
 static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, const int* src, const int* dst, bool bwd,
@@ -267,7 +281,7 @@ static BfBuf at(const BfBuf& b, long long elem) { return BfBuf{b.p + elem, b.lo}
 // Hin = 0 computes only that column sum.
 static void wgrad(xmgn_workspace* ws, const BfBuf& a0, const BfBuf& a1, int a_width, int a_split_tiles, const BfBuf& b,
                   int b_width, int b_col0, long long rows, int Hin, float* grad, long long dst, cudaStream_t st,
-                  long long bias_dst = -1) {
+                  long long bias_dst = -1, const float* inv = nullptr) {
   if (rows <= 0) return;
   const int H = ws->H;
   WgradParams p;
@@ -304,8 +318,9 @@ static void wgrad(xmgn_workspace* ws, const BfBuf& a0, const BfBuf& a1, int a_wi
   }
   XMGN_CUDA(cudaGetLastError(), "wgrad launch");
   const long long ld = (long long)(Hin + (p.ones_tile ? 128 : 0)) * H;
-  if (Hin > 0) launch_reduce_part(ws->part, S, (long long)Hin * H, ld, grad + dst, st, ws->d_scale + 1);
-  if (p.ones_tile) launch_reduce_part(ws->part + (long long)Hin * H, S, H, ld, grad + bias_dst, st, ws->d_scale + 1);
+  if (!inv) inv = ws->d_scale + 1;
+  if (Hin > 0) launch_reduce_part(ws->part, S, (long long)Hin * H, ld, grad + dst, st, inv);
+  if (p.ones_tile) launch_reduce_part(ws->part + (long long)Hin * H, S, H, ld, grad + bias_dst, st, inv);
 }
 
 static void colsum_reduce(xmgn_workspace* ws, int blk, int l, float* grad, int grid_used, cudaStream_t st,
@@ -463,14 +478,12 @@ static inline int64_t n_at(const Part& P, int L, int l) {  // rows of layer l (r
 }
 static inline int64_t e_at(const Part& P, int L, int l) { return P.ring_edges[L - l + 1]; }
 
-extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const float* params, const float* h0,
-                                          const float* e0, float* h_out, void* stream) {
-  return guarded("xmgn_processor_fwd", [&]() -> xmgn_status {
-    if (!ws || !params || !h0 || !e0 || !h_out) return set_error(XMGN_EINVAL, "xmgn_processor_fwd: null argument");
-    if (part < 0 || part >= (int)ws->g->parts.size())
-      return set_error(XMGN_EINVAL, "xmgn_processor_fwd: part=%d outside [0,%d)", part, (int)ws->g->parts.size());
-    XMGN_CUDA(cudaSetDevice(ws->dev), "xmgn_processor_fwd: cudaSetDevice");
-    cudaStream_t st = (cudaStream_t)stream;
+// The processor forward of partition `part`.  staged: the encoders (xmgn_model_fwd) already
+// wrote h^0 (FP32 h0 = h_buf[0] and its 16-bit copy h_ck[0]) and e^0 (16-bit e_ck[0], FP32 e0 =
+// e32[0] in the BF16 mode); hL16 (may be null): also write h^L of the owned rows in 16 bits.
+static void proc_fwd(xmgn_workspace* ws, int part, const float* params, const float* h0, const float* e0,
+                     float* h_out, bool staged, bf16* hL16, cudaStream_t st) {
+  {
     const Part& P = ws->g->parts[part];
     const DPart& dp = ws->dparts[part];
     const int H = ws->H, L = ws->L, m = ws->m;
@@ -478,8 +491,10 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
     Layout Ly{H, L, m};
     launch_pack(ws->f16, params, ws->d_jobs, ws->njobs, st);
     const int64_t n0 = n_at(P, L, 0), e1 = e_at(P, L, 1);
-    launch_to_bf16(ws->f16, h0, ws->h_ck.p, ws->h_ck.lo, n0 * H, st);
-    launch_to_bf16(ws->f16, e0, ws->e_ck.p, ws->e_ck.lo, e1 * H, st);
+    if (!staged) {
+      launch_to_bf16(ws->f16, h0, ws->h_ck.p, ws->h_ck.lo, n0 * H, st);
+      launch_to_bf16(ws->f16, e0, ws->e_ck.p, ws->e_ck.lo, e1 * H, st);
+    }
     const int W1 = 0, W2 = 2;  // weight map slots
     auto r1 = [&](int l, int slot) { return (l * ws->S1 + slot) * H; };
     auto r2 = [&](int l, int slot) { return (l * ws->S2 + slot) * H; };
@@ -560,6 +575,10 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
         s.gamma = params + Ly.gamma(li, 1); s.beta = params + Ly.beta(li, 1);
         s.f_in = h_in; s.ld_in = H; s.f_out = hn; s.ld_out = H;
         s.flags = EF_STORE_F32;
+        if (l == L && hL16) {
+          s.flags |= EF_STORE_BF;
+          s.bf_out = hL16; s.bf_lo = 0;
+        }
         if (l < L) {
           s.flags |= EF_STORE_BF | EF_WRITE_ACT;
           s.bf_out = ws->h_ck.p + ws->ck(l) * NH; s.bf_lo = ws->h_ck.lo;
@@ -575,6 +594,18 @@ extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const fl
       cur ^= 1;
     }
     ws->last_fwd = part;
+  }
+}
+
+extern "C" xmgn_status xmgn_processor_fwd(xmgn_workspace* ws, int part, const float* params, const float* h0,
+                                          const float* e0, float* h_out, void* stream) {
+  return guarded("xmgn_processor_fwd", [&]() -> xmgn_status {
+    if (!ws || !params || !h0 || !e0 || !h_out) return set_error(XMGN_EINVAL, "xmgn_processor_fwd: null argument");
+    if (part < 0 || part >= (int)ws->g->parts.size())
+      return set_error(XMGN_EINVAL, "xmgn_processor_fwd: part=%d outside [0,%d)", part, (int)ws->g->parts.size());
+    XMGN_CUDA(cudaSetDevice(ws->dev), "xmgn_processor_fwd: cudaSetDevice");
+    ws->last_model_fwd = -1;
+    proc_fwd(ws, part, params, h0, e0, h_out, false, nullptr, (cudaStream_t)stream);
     return XMGN_OK;
   });
 }
@@ -700,6 +731,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
                 Ly.b(li, 0, j));
         wgrad(ws, none, none, H, 0, ws->Ge[gc], H, 0, el, 0, grad_params, 0, st, Ly.beta(li, 0));
         gc ^= 1;   // G_e^{l-1} now lives in the other buffer
+        ws->gc_last = gc;
       }
       // D = [sum over out-edges | sum over in-edges] of dZ0 (adjoint of the P gathers)
       { ProfScope ps("segsum", st);
@@ -727,6 +759,298 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
       launch_to_f32(ws->f16, ws->Ge[gc].p, ws->Ge[gc].lo, grad_e0, e1 * H, st, ws->d_scale + 1);
       if (P.e_local > e1)
         XMGN_CUDA(cudaMemsetAsync(grad_e0 + e1 * H, 0, (P.e_local - e1) * H * sizeof(float), st), "grad_e0");
+    }
+    return XMGN_OK;
+  });
+}
+
+// ================================================================ the model around the processor (NEXT-1)
+// encoders -> processor -> decoder -> owned-row MSE (PAPER.md:161, 197, 219,
+// 234).  The encoders' and decoder's H x H layers run as k_chain programs on the tensor cores (the
+// encoders' first layer with K = 64: the 24 / 4 inputs zero-padded to one operand box); the
+// decoder's 4-wide output layer, the loss and the encoders' first-layer weight gradient are thin
+// CUDA-core kernels (io_kernels.cu).
+namespace xmgn {
+
+// IO parameter layout (include/xmgn.h; restated independently of oracle/model.py): node encoder,
+// edge encoder [W_0 (F x H), b_0, W_j (H x H), b_j for j = 1..m, gamma, beta], decoder [W_0, b_0,
+// ..., W_{m-1}, b_{m-1} (H x H), W_m (H x 4), b_m (4)].  blk 0 / 1 / 2 = node enc / edge enc / dec.
+struct IoLayout {
+  int H, m;
+  int fin(int blk) const { return blk == 0 ? IO_F_NODE : IO_F_EDGE; }
+  int64_t kin(int blk, int j) const { return j == 0 && blk < 2 ? fin(blk) : H; }
+  int64_t nout(int blk, int j) const { return blk == 2 && j == m ? IO_DOUT : H; }
+  int64_t lin(int blk, int j) const { return kin(blk, j) * nout(blk, j) + nout(blk, j); }
+  int64_t size(int blk) const {
+    int64_t o = blk < 2 ? 2 * (int64_t)H : 0;
+    for (int j = 0; j <= m; ++j) o += lin(blk, j);
+    return o;
+  }
+  int64_t base(int blk) const { return blk == 0 ? 0 : (blk == 1 ? size(0) : size(0) + size(1)); }
+  int64_t W(int blk, int j) const {
+    int64_t o = base(blk);
+    for (int i = 0; i < j; ++i) o += lin(blk, i);
+    return o;
+  }
+  int64_t b(int blk, int j) const { return W(blk, j) + kin(blk, j) * nout(blk, j); }
+  int64_t gamma(int blk) const { return b(blk, m) + H; }
+  int64_t beta(int blk) const { return gamma(blk) + H; }
+  int64_t count() const { return base(2) + size(2); }
+};
+// wioH slots of H rows: encoder blk: W_j^T at 2m blk + j - 1, W_j (dgrad) at 2m blk + m + j - 1
+// (j = 1..m); decoder: W_j^T at 4m + j, W_j at 5m + j (j = 0..m-1)
+static long long io_T(int m, int blk, int j) { return blk < 2 ? 2 * m * blk + j - 1 : 4 * m + j; }
+static long long io_D(int m, int blk, int j) { return blk < 2 ? 2 * m * blk + m + j - 1 : 5 * m + j; }
+
+static void ensure_io(xmgn_workspace* ws) {
+  if (ws->io_ready) return;
+  const int H = ws->H, m = ws->m;
+  for (const Part& P : ws->g->parts) ws->Omax = std::max(ws->Omax, P.n_owned);
+  const int64_t O = std::max<int64_t>(ws->Omax, 1);
+  IoLayout Io{H, m};
+  ws->S3 = 6 * m;
+  ws->wio64 = bfalloc(ws, (size_t)2 * H * IO_IN_COLS);
+  XMGN_CUDA(cudaMemset(ws->wio64.p, 0, (size_t)2 * H * IO_IN_COLS * sizeof(bf16)), "io weights");  // K padding
+  ws->wioH = bfalloc(ws, (size_t)ws->S3 * H * H);
+  std::vector<PackJob> J;
+  auto job = [&](BfBuf& buf, int ld, long long row0, int rows, int cols, long long src, long long sr, long long sc) {
+    PackJob j;
+    j.dst = buf.p + row0 * ld;
+    j.lo_off = 0;
+    j.ld = ld; j.rows = rows; j.cols = cols; j.src = src; j.sr = sr; j.sc = sc;
+    J.push_back(j);
+  };
+  for (int blk = 0; blk < 2; ++blk) {
+    job(ws->wio64, IO_IN_COLS, (long long)blk * H, H, Io.fin(blk), Io.W(blk, 0), 1, H);
+    for (int j = 1; j <= m; ++j) {
+      job(ws->wioH, H, io_T(m, blk, j) * H, H, H, Io.W(blk, j), 1, H);
+      job(ws->wioH, H, io_D(m, blk, j) * H, H, H, Io.W(blk, j), H, 1);
+    }
+  }
+  for (int j = 0; j < m; ++j) {
+    job(ws->wioH, H, io_T(m, 2, j) * H, H, H, Io.W(2, j), 1, H);
+    job(ws->wioH, H, io_D(m, 2, j) * H, H, H, Io.W(2, j), H, 1);
+  }
+  ws->njobs_io = (int)J.size();
+  ws->d_jobs_io = (PackJob*)dalloc(ws, J.size() * sizeof(PackJob));
+  XMGN_CUDA(cudaMemcpy(ws->d_jobs_io, J.data(), J.size() * sizeof(PackJob), cudaMemcpyHostToDevice), "upload");
+  ws->Xn = bfalloc(ws, (size_t)std::max<int64_t>(ws->Nmax, 1) * IO_IN_COLS);
+  ws->Xe = bfalloc(ws, (size_t)std::max<int64_t>(ws->Emax, 1) * IO_IN_COLS);
+  ws->hL16 = bfalloc(ws, (size_t)O * H);
+  ws->zdec = (float*)dalloc(ws, (size_t)O * H * 4);
+  ws->sse_part = (double*)dalloc(ws, (size_t)dec_head_warps(O) * sizeof(double));
+  if (!ws->infer) {
+    ws->dZdec = bfalloc(ws, (size_t)O * H);
+    ws->gdec = (float*)dalloc(ws, (size_t)O * H * 4);
+    ws->wpart = (float*)dalloc(ws, (size_t)dec_head_warps(O) * (H * IO_DOUT + IO_DOUT) * 4);
+    ws->thin_part = (float*)dalloc(ws, (size_t)wgrad_thin_blocks(std::max(ws->Nmax, ws->Emax)) * IO_F_NODE * H * 4);
+    ws->d_scale_dec = (float*)dalloc(ws, 2 * sizeof(float));
+  }
+  ws->io_ready = true;
+}
+
+static int weight_map(xmgn_workspace* ws, Prog& pr, const bf16* base, int width, long long rows) {
+  if (pr.next_map >= MAX_MAPS) throw Fail{set_error(XMGN_ESTATE, "internal: out of tensor-map slots")};
+  const int NB = (ws->H < 256 ? ws->H : 256) / 2;
+  pr.p.maps[pr.next_map] = tmap16(base, width, rows, width, 64, NB, ws->f16);
+  return pr.next_map++;
+}
+
+// encoder blk (0 node, 1 edge) over rows [0, rows) of its 16-bit inputs X: forward (bwd = false:
+// y = LN(MLP(X)) -> h^0 / e^0) or recompute + backward (bwd = true: dZ_j into scrZ[j], A_j / S'_j
+// into scrA / scrS, column sums for gamma, beta and the biases)
+static void enc_prog(xmgn_workspace* ws, int blk, const float* io, long long rows, bool bwd, cudaStream_t st) {
+  if (rows <= 0) return;
+  const int H = ws->H, m = ws->m;
+  IoLayout Io{H, m};
+  const BfBuf& X = blk ? ws->Xe : ws->Xn;
+  Prog pr(ws);
+  pr.p.maps[4] = map_rows(X.p, rows, IO_IN_COLS, 128, ws->f16);
+  pr.p.maps[5] = pr.p.maps[4];
+  const int w64 = weight_map(ws, pr, ws->wio64.p, IO_IN_COLS, 2LL * H);
+  const int wH = weight_map(ws, pr, ws->wioH.p, H, (long long)ws->S3 * H);
+  for (int j = 0; j < m; ++j) {
+    Step& s = pr.add();
+    s.a_src = j ? A_ACT : A_TMA; s.a_map0 = 4; s.K = j ? H : IO_IN_COLS;
+    s.b_map = j ? wH : w64; s.b_row0 = (int)(j ? io_T(ws->m, blk, j) * H : (long long)blk * H);
+    s.epi = EPI_SILU; s.bias = io + Io.b(blk, j);
+    if (bwd) {
+      s.flags = EF_STORE_A | EF_STORE_S; s.scr_a = ws->scrA[j].p; s.scr_s = ws->scrS[j].p; s.lo_off = 0;
+      s.st_map = pr.in_map(ws->scrA[j].p, rows, H);
+    }
+  }
+  Step& s = pr.add();
+  s.a_src = m ? A_ACT : A_TMA; s.a_map0 = 4; s.K = H; s.b_map = wH; s.b_row0 = (int)(io_T(m, blk, m) * H);
+  s.bias = io + Io.b(blk, m); s.gamma = io + Io.gamma(blk); s.beta = io + Io.beta(blk);
+  if (!bwd) {
+    s.epi = EPI_LN_FWD; s.flags = EF_NO_RES | EF_STORE_BF; s.bf_lo = 0;
+    if (blk == 0) { s.flags |= EF_STORE_F32; s.f_out = ws->h_buf[0]; s.ld_out = H; s.bf_out = ws->h_ck.p; }
+    else {
+      s.bf_out = ws->e_ck.p;
+      if (ws->e32_mode) { s.flags |= EF_STORE_F32; s.f_out = ws->e32[0]; s.ld_out = H; }
+    }
+    run_prog(ws, blk ? "enc_edge_fwd" : "enc_node_fwd", pr, (int)rows, nullptr, nullptr, false, st);
+    return;
+  }
+  s.epi = EPI_LN_BWD; s.flags = EF_COLSUM_ALL;
+  if (blk == 0) { s.f_in = ws->Gh; s.ld_in = H; s.valid_in = (int)rows; }
+  else {
+    s.flags |= EF_G16 | EF_NO_GA; s.g16 = ws->Ge[ws->gc_last].p; s.g16_lo = 0; s.valid_in = (int)rows;
+    s.in_map = pr.in_map(ws->Ge[ws->gc_last].p, rows, H);
+  }
+  s.scr_z = ws->scrZ[m].p; s.lo_off = 0; s.st_map = pr.in_map(ws->scrZ[m].p, rows, H);
+  for (int j = m; j >= 1; --j) {
+    Step& d = pr.add();
+    d.a_src = A_ACT; d.K = H; d.b_map = wH; d.b_row0 = (int)(io_D(m, blk, j) * H);
+    d.epi = EPI_DSILU; d.flags = EF_COLSUM_ALL | EF_DISCARD; d.vec0 = 3 + (m - j);
+    d.scr_s = ws->scrS[j - 1].p; d.scr_z = ws->scrZ[j - 1].p; d.lo_off = 0;
+    d.in_map = pr.in_map(ws->scrS[j - 1].p, rows, H);
+    if (j > 1) d.st_map = pr.in_map(ws->scrZ[j - 1].p, rows, H);
+    else d.flags |= EF_NO_ACT;   // dZ_0 by row stores: the program must not end writing ACT
+  }
+  run_prog(ws, blk ? "enc_edge_bwd" : "enc_node_bwd", pr, (int)rows, nullptr, nullptr, true, st);
+}
+
+}  // namespace xmgn
+
+extern "C" size_t xmgn_io_param_count(const xmgn_model_cfg* c) {
+  if (!c || c->hidden <= 0 || c->mlp_hidden_layers < 1) return 0;
+  return (size_t)IoLayout{c->hidden, c->mlp_hidden_layers}.count();
+}
+
+extern "C" xmgn_status xmgn_model_fwd(xmgn_workspace* ws, int part, const float* params, const float* io_params,
+                                      const float* pos, const float* nrm, const float* stats, const float* targets,
+                                      int64_t n_global, float* pred, float* loss, void* stream) {
+  return guarded("xmgn_model_fwd", [&]() -> xmgn_status {
+    if (!ws || !params || !io_params || !pos || !nrm || !stats || !pred)
+      return set_error(XMGN_EINVAL, "xmgn_model_fwd: null argument");
+    if (part < 0 || part >= (int)ws->g->parts.size())
+      return set_error(XMGN_EINVAL, "xmgn_model_fwd: part=%d outside [0,%d)", part, (int)ws->g->parts.size());
+    if (ws->split) return set_error(XMGN_EUNSUPPORTED, "xmgn_model_fwd: the FP32 check mode covers the processor only");
+    const Part& P = ws->g->parts[part];
+    if (targets && (!loss || n_global < P.n_owned || n_global <= 0))
+      return set_error(XMGN_EINVAL, "xmgn_model_fwd: targets need loss != NULL and n_global=%lld >= n_owned=%lld > 0",
+                       (long long)n_global, (long long)P.n_owned);
+    XMGN_CUDA(cudaSetDevice(ws->dev), "xmgn_model_fwd: cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    ensure_io(ws);
+    const DPart& dp = ws->dparts[part];
+    const int H = ws->H, L = ws->L, m = ws->m;
+    IoLayout Io{H, m};
+    const float* io = io_params;
+    launch_pack(ws->f16, io, ws->d_jobs_io, ws->njobs_io, st);
+    const int64_t n0 = n_at(P, L, 0), e1 = e_at(P, L, 1), no = P.n_owned;
+    // inputs and encoders -> h^0, e^0
+    launch_node_inputs(ws->f16, pos, nrm, stats, n0, ws->Xn.p, st);
+    launch_edge_inputs(ws->f16, pos, dp.src, dp.dst, stats, e1, ws->Xe.p, st);
+    enc_prog(ws, 0, io, n0, false, st);
+    enc_prog(ws, 1, io, e1, false, st);
+    // processor (h^L of the owned rows also in 16 bits for the decoder)
+    proc_fwd(ws, part, params, ws->h_buf[0], ws->e32_mode ? ws->e32[0] : nullptr, ws->h_buf[L & 1], true, ws->hL16.p,
+             st);
+    // decoder hidden layers on the tensor cores -> zdec = A_{m-1} W_{m-1} (bias added by the head)
+    const bool train = !ws->infer && targets;
+    {
+      Prog pr(ws);
+      set_a(ws, pr, 4, ws->hL16, no, H);
+      const int wH = weight_map(ws, pr, ws->wioH.p, H, (long long)ws->S3 * H);
+      for (int j = 0; j < m; ++j) {
+        Step& s = pr.add();
+        s.a_src = j ? A_ACT : A_TMA; s.a_map0 = 4; s.K = H; s.b_map = wH; s.b_row0 = (int)(io_T(m, 2, j) * H);
+        if (j < m - 1) {
+          s.epi = EPI_SILU; s.bias = io + Io.b(2, j);
+          if (train && no > 0) {
+            s.flags = EF_STORE_A | EF_STORE_S; s.scr_a = ws->scrA[j].p; s.scr_s = ws->scrS[j].p; s.lo_off = 0;
+            s.st_map = pr.in_map(ws->scrA[j].p, no, H);
+          }
+        } else {
+          s.epi = EPI_STORE; s.f_out = ws->zdec; s.ld_out = H; s.col0 = 0;
+        }
+      }
+      run_prog(ws, "dec_fwd", pr, (int)no, nullptr, nullptr, false, st);
+    }
+    // output layer + owned-row MSE (+ its adjoint for the backward)
+    const double nd = (double)IO_DOUT * (double)(n_global > 0 ? n_global : 1);
+    const float inv_nd = (float)(1.0 / nd);
+    const float S = (float)std::ldexp(1.0, (int)std::floor(std::log2(nd)));   // dy S = O(y - t)
+    ws->head_warps = dec_head_warps(std::max<int64_t>(no, 1));
+    launch_dec_head(ws->f16, H, ws->zdec, no, io + Io.b(2, m - 1), io + Io.W(2, m), io + Io.b(2, m), targets, inv_nd, S,
+                    pred, ws->sse_part, train ? ws->dZdec.p : nullptr, ws->wpart, st);
+    if (targets && no > 0) launch_loss_reduce(ws->sse_part, ws->head_warps, inv_nd, loss, st);
+    if (train) {
+      launch_set_scale(ws->d_scale_dec, S, 1.0f / S, st);
+      ws->last_model_fwd = part;
+    } else {
+      ws->last_model_fwd = -1;
+    }
+    return XMGN_OK;
+  });
+}
+
+extern "C" xmgn_status xmgn_model_bwd(xmgn_workspace* ws, int part, const float* params, const float* io_params,
+                                      float* grad_params, float* grad_io, void* stream) {
+  return guarded("xmgn_model_bwd", [&]() -> xmgn_status {
+    if (!ws || !params || !io_params || !grad_params || !grad_io)
+      return set_error(XMGN_EINVAL, "xmgn_model_bwd: null argument");
+    if (ws->infer) return set_error(XMGN_ESTATE, "xmgn_model_bwd: inference workspace");
+    if (part != ws->last_model_fwd || part != ws->last_fwd)
+      return set_error(XMGN_ESTATE, "xmgn_model_bwd: part=%d is not the last xmgn_model_fwd with targets (%d)", part,
+                       ws->last_model_fwd);
+    XMGN_CUDA(cudaSetDevice(ws->dev), "xmgn_model_bwd: cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    const Part& P = ws->g->parts[part];
+    const int H = ws->H, L = ws->L, m = ws->m;
+    IoLayout Io{H, m};
+    const float* io = io_params;
+    const int64_t no = P.n_owned;
+    const BfBuf none{};
+    // decoder backward: S dZ_{m-1} (head) -> dgrad chain -> S dL/dh^L (FP32)
+    {
+      Prog pr(ws);
+      set_a(ws, pr, 4, ws->dZdec, no, H);
+      const int wH = weight_map(ws, pr, ws->wioH.p, H, (long long)ws->S3 * H);
+      for (int j = m - 1; j >= 0; --j) {
+        Step& s = pr.add();
+        s.a_src = j == m - 1 ? A_TMA : A_ACT; s.a_map0 = 4; s.K = H; s.b_map = wH; s.b_row0 = (int)(io_D(m, 2, j) * H);
+        if (j > 0) {
+          s.epi = EPI_DSILU; s.scr_s = ws->scrS[j - 1].p; s.scr_z = ws->scrZ[j - 1].p; s.lo_off = 0;
+          if (no > 0) { s.in_map = pr.in_map(ws->scrS[j - 1].p, no, H); s.st_map = pr.in_map(ws->scrZ[j - 1].p, no, H); }
+        } else {
+          s.epi = EPI_STORE; s.f_out = ws->gdec; s.ld_out = H; s.col0 = 0;
+        }
+      }
+      run_prog(ws, "dec_bwd", pr, (int)no, nullptr, nullptr, true, st);
+    }
+    auto dZ = [&](int j) { return j == m - 1 ? ws->dZdec : ws->scrZ[j]; };
+    const float* inv_dec = ws->d_scale_dec + 1;
+    for (int j = m - 1; j >= 1; --j)   // dW_j = A_{j-1}^T dZ_j, db_j (ones tile)
+      wgrad(ws, ws->scrA[j - 1], none, H, H / 128, dZ(j), H, 0, no, H, grad_io, Io.W(2, j), st, Io.b(2, j), inv_dec);
+    wgrad(ws, ws->hL16, none, H, H / 128, dZ(0), H, 0, no, H, grad_io, Io.W(2, 0), st, Io.b(2, 0), inv_dec);
+    if (no > 0) {
+      const long long nw = (long long)H * IO_DOUT + IO_DOUT;   // dW_m [H x 4] then db_m [4]
+      launch_reduce_part(ws->wpart, ws->head_warps, nw, nw, grad_io + Io.W(2, m), st, nullptr);
+      launch_scale_copy(ws->gdec, no * H, inv_dec, ws->gdec, st);
+    }
+    // processor backward (its own exact loss scale S_p: Gh, G_e come out x S_p)
+    xmgn_status r = xmgn_processor_bwd(ws, part, params, ws->gdec, grad_params, nullptr, nullptr, stream);
+    if (r != XMGN_OK) return r;
+    // encoders: upstream dL/dh^0 (Gh) and dL/de^0 (G_e), both x S_p
+    const int64_t n0 = n_at(P, L, 0), e1 = e_at(P, L, 1);
+    for (int blk = 0; blk < 2; ++blk) {
+      const long long rows = blk ? e1 : n0;
+      if (rows <= 0) continue;
+      enc_prog(ws, blk, io, rows, true, st);
+      ColsumDst d;
+      for (int v = 0; v < NV_MAX; ++v) d.off[v] = -1;
+      d.off[0] = Io.gamma(blk); d.off[1] = Io.beta(blk); d.off[2] = Io.b(blk, m); d.off[3] = Io.b(blk, m - 1);
+      if (m >= 2) d.off[4] = Io.b(blk, m - 2);
+      launch_reduce_colsum(ws->colsum, chain_grid(ws, (int)rows), NV_MAX, H, d, grad_io, st, ws->d_scale + 1);
+      for (int j = 1; j <= m; ++j)
+        wgrad(ws, ws->scrA[j - 1], none, H, H / 128, ws->scrZ[j], H, 0, rows, H, grad_io, Io.W(blk, j), st);
+      const BfBuf& X = blk ? ws->Xe : ws->Xn;
+      const long long nf = (long long)Io.fin(blk) * H;
+      launch_wgrad_thin(ws->f16, Io.fin(blk), X.p, ws->scrZ[0].p, rows, H, ws->thin_part, st);
+      launch_reduce_part(ws->thin_part, wgrad_thin_blocks(rows), nf, nf, grad_io + Io.W(blk, 0), st, ws->d_scale + 1);
     }
     return XMGN_OK;
   });

@@ -75,6 +75,27 @@ class Processor:
             gids.append(self.info[p]["gid"][:self.info[p]["n_owned"]])
         return torch.cat(outs), np.concatenate(gids)
 
+    # ------------------------------------------------------------------ the full model (NEXT-1)
+    def make_model_inputs(self, p, bundle):
+        """pos, nrm [n_local, 3] (local order) and z-scored targets [n_owned, 4] on the device."""
+        inf = self.info[p]
+        gid = inf["gid"]
+        pos = torch.as_tensor(np.ascontiguousarray(bundle["positions"][gid], np.float32), device=self.device)
+        nrm = torch.as_tensor(np.ascontiguousarray(bundle["normals"][gid], np.float32), device=self.device)
+        t = tensors.targets(torch.as_tensor(gid[:inf["n_owned"]], device=self.device), self.device)
+        return pos, nrm, t
+
+    def make_io_params(self):
+        return tensors.io_params(self.H, self.m, self.device)
+
+    def model_forward(self, p, params, io_params, pos, nrm, stats, targets=None, n_global=0, loss=None, stream=None):
+        pred = torch.empty((self.info[p]["n_owned"], xmgn.IO_DOUT), dtype=torch.float32, device=self.device)
+        self.ws.model_forward(p, params, io_params, pos, nrm, stats, pred, targets, n_global, loss, stream)
+        return pred
+
+    def model_backward(self, p, params, io_params, grad_params, grad_io, stream=None):
+        self.ws.model_backward(p, params, io_params, grad_params, grad_io, stream)
+
     def close(self):
         self.ws.close()
         self.graph.close()

@@ -81,6 +81,9 @@ _sig("xmgn_scatter_rows", _i32, [_vp, _vp, _i64, _i64, _vp, _vp])
 _sig("xmgn_cosine_lr", ctypes.c_float, [ctypes.POINTER(AdamCfg), _i64])
 _sig("xmgn_adam_step", _i32, [ctypes.POINTER(AdamCfg), _i64, _vp, _vp, _vp, _vp, _sz, ctypes.c_float, _vp, _vp])
 _sig("xmgn_selftest_gemm", _i32, [_i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp])
+_sig("xmgn_io_param_count", _sz, [ctypes.POINTER(ModelCfg)])
+_sig("xmgn_model_fwd", _i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp])
+_sig("xmgn_model_bwd", _i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp])
 _sig("xmgn_launch_count", ctypes.c_longlong, [])
 _sig("xmgn_profile_enable", _i32, [_i32])
 _sig("xmgn_profile_collect", _i32, [ctypes.c_char_p, _sz, ctypes.POINTER(ctypes.c_double),
@@ -92,6 +95,7 @@ EXPORTS = ["xmgn_last_error", "xmgn_version", "xmgn_load_graph", "xmgn_part_info
            "xmgn_workspace_free", "xmgn_processor_fwd", "xmgn_processor_bwd", "xmgn_check_finite",
            "xmgn_comm_unique_id", "xmgn_comm_init", "xmgn_grad_reduce", "xmgn_comm_destroy", "xmgn_gather_rows",
            "xmgn_scatter_rows",
+           "xmgn_io_param_count", "xmgn_model_fwd", "xmgn_model_bwd",
            "xmgn_cosine_lr", "xmgn_adam_step", "xmgn_selftest_gemm", "xmgn_launch_count", "xmgn_profile_enable", "xmgn_profile_collect"]
 
 
@@ -180,6 +184,13 @@ def param_count(cfg):
     return int(_lib.xmgn_param_count(ctypes.byref(cfg)))
 
 
+def io_param_count(cfg):
+    return int(_lib.xmgn_io_param_count(ctypes.byref(cfg)))
+
+
+IO_NSTATS, IO_DOUT = 56, 4   # [mean | std] of the 24 node + 4 edge inputs; outputs per node
+
+
 def _dev_f32(t, name, numel, device=None):
     """Device pointer of a CUDA, float32, contiguous torch tensor holding at least
     `numel` values (the library reads / writes exactly that many)."""
@@ -242,6 +253,27 @@ class Workspace:
                                        _dev_f32(grad_params, "grad_params", self.n_params, dv),
                                        _dev_f32(grad_h0, "grad_h0", nl * H, dv),
                                        _dev_f32(grad_e0, "grad_e0", el * H, dv), _stream(stream)))
+
+    def model_forward(self, part, params, io_params, pos, nrm, stats, pred, targets=None, n_global=0, loss=None,
+                      stream=None):
+        """xmgn_model_fwd: encoders -> processor -> decoder (-> owned-row MSE with targets)."""
+        no, nl, el = self._sizes(part)
+        dv = self.graph.device
+        nio = io_param_count(self.cfg)
+        _check(_lib.xmgn_model_fwd(self.handle, int(part), _dev_f32(params, "params", self.n_params, dv),
+                                   _dev_f32(io_params, "io_params", nio, dv), _dev_f32(pos, "pos", nl * 3, dv),
+                                   _dev_f32(nrm, "nrm", nl * 3, dv), _dev_f32(stats, "stats", IO_NSTATS, dv),
+                                   _dev_f32(targets, "targets", no * IO_DOUT, dv), int(n_global),
+                                   _dev_f32(pred, "pred", no * IO_DOUT, dv), _dev_f32(loss, "loss", 1, dv),
+                                   _stream(stream)))
+
+    def model_backward(self, part, params, io_params, grad_params, grad_io, stream=None):
+        dv = self.graph.device
+        nio = io_param_count(self.cfg)
+        _check(_lib.xmgn_model_bwd(self.handle, int(part), _dev_f32(params, "params", self.n_params, dv),
+                                   _dev_f32(io_params, "io_params", nio, dv),
+                                   _dev_f32(grad_params, "grad_params", self.n_params, dv),
+                                   _dev_f32(grad_io, "grad_io", nio, dv), _stream(stream)))
 
     def close(self):
         if getattr(self, "handle", None) and _lib is not None:
