@@ -192,6 +192,32 @@ xmgn_status xmgn_model_fwd(xmgn_workspace* ws, int part, const float* params, co
 xmgn_status xmgn_model_bwd(xmgn_workspace* ws, int part, const float* params, const float* io_params,
                            float* grad_params, float* grad_io, void* stream);
 
+/* ------------------------------------------------------------------ graph construction on the GPU (NEXT-4)
+ * The step before the hot path (Sec. III-B/C): from a point cloud
+ * whose levels are prefix-nested (level l = points [0, level_counts[l]), "the point
+ * cloud from the previous scale is a subset of the point cloud at the next finer scale"):
+ *  - per level, edges (j -> i) for the k nearest j != i (k capped at level size - 1), d^2 in FP64
+ *    from the FP32 positions as ((dx dx) + (dy dy)) + dz dz, ties to the smaller index;
+ *  - symmetrised, united over the levels, deduplicated: CSR by destination, sources ascending;
+ *  - n_parts partitions by recursive coordinate bisection (the axis of largest extent, nodes ordered
+ *    by (coordinate, id), left part round-half-even(len * floor(p/2) / p) nodes) -- the stand-in for
+ *    METIS;
+ *  - per partition the halo: nodes within halo_depth undirected hops of its owned set, ordered by
+ *    (ring, id) ("equal to the number of message passing layers").
+ * pos: device FP32 [n_nodes, 3] on cuda_device; level_counts: host, strictly increasing, last =
+ * n_nodes; 1 <= k <= 16; 1 <= n_parts <= n_nodes; 0 <= halo_depth <= 63.  Runs on `stream` and
+ * returns when the result (host arrays owned by the handle) is complete.  The result is bitwise
+ * the construction of oracle/graphbuild.py.  EINVAL on malformed arguments.                  */
+typedef struct xmgn_built_graph xmgn_built_graph;
+xmgn_status xmgn_build_graph(const float* pos, int64_t n_nodes, const int64_t* level_counts, int n_levels, int k,
+                             int n_parts, int halo_depth, int cuda_device, void* stream, xmgn_built_graph** out);
+/* A descriptor pointing into the handle's host arrays (valid until xmgn_built_graph_free), ready
+ * for xmgn_load_graph.                                                                        */
+xmgn_status xmgn_built_graph_desc(const xmgn_built_graph* b, xmgn_graph_desc* desc);
+/* owner[n_nodes] (host, caller-allocated): the partition of every node.                       */
+xmgn_status xmgn_built_graph_owner(const xmgn_built_graph* b, int64_t* owner);
+void xmgn_built_graph_free(xmgn_built_graph* b);
+
 /* ------------------------------------------------------------------ gradient aggregation
  * One NCCL communicator per process/GPU (one process per GPU).  The unique id
  * is created on rank 0 and broadcast by the caller (e.g. torch.distributed).

@@ -3,12 +3,16 @@
 #include <atomic>
 #include "kernels_launch.h"
 
+#ifndef XMGN_OPS_SPECIALISE
+#define XMGN_OPS_SPECIALISE 1
+#endif
+
 namespace xmgn {
 
-template <int H, bool SPLIT, bool BWD, bool F16, bool Z1 = false, bool PIPE = false>
+template <int H, bool SPLIT, bool BWD, bool F16, bool Z1 = false, bool PIPE = false, int OPS = OPS_ALL>
 static void chain_launch(const ChainParams& p, int grid, cudaStream_t st) {
   using C = ChainCfg<H, SPLIT>;
-  auto kern = k_chain<H, SPLIT, BWD, F16, Z1, PIPE>;
+  auto kern = k_chain<H, SPLIT, BWD, F16, Z1, PIPE, OPS>;
   // the smem attribute is per device context: one flag per device (set idempotently,
   // so two host threads racing on the same device are harmless)
   static std::atomic<bool> attr[64];
@@ -33,6 +37,13 @@ static void launch_h(bool bwd, bool pipe, const ChainParams& p, int grid, cudaSt
   for (int i = 0; i < p.n_steps; ++i) z1 = z1 || (p.steps[i].flags & EF_FROM_IN) != 0;
   if constexpr (H == 512) {
     if (pipe && !z1) {
+      // the edge programs get kernels holding only their ops (XMGN_OPS_SPECIALISE=0: off)
+      int ops = 0;
+      for (int i = 0; i < p.n_steps; ++i) ops |= step_opbit(p.steps[i]);
+#if XMGN_OPS_SPECIALISE
+      if (bwd && (ops & ~OPS_EDGE_BWD) == 0) { chain_launch<H, false, true, F16, false, true, OPS_EDGE_BWD>(p, grid, st); return; }
+      if (!bwd && (ops & ~OPS_EDGE_FWD) == 0) { chain_launch<H, false, false, F16, false, true, OPS_EDGE_FWD>(p, grid, st); return; }
+#endif
       if (bwd) chain_launch<H, false, true, F16, false, true>(p, grid, st);
       else chain_launch<H, false, false, F16, false, true>(p, grid, st);
       return;

@@ -114,6 +114,26 @@ __host__ __device__ inline bool step_uses_act(const Step& st) {
   return step_writes_act(st) || st.in_map >= 0 || st.gsrc_map >= 0 || st.st_map >= 0;
 }
 
+// epilogue ops a kernel instantiation contains (OPS template mask): the hot programs get kernels
+// without the code of ops they never run (smaller instruction footprint)
+enum : int {
+  OPB_SILU = 1, OPB_LNF16 = 2, OPB_LNF32 = 4, OPB_STORE = 8, OPB_ADD16 = 16, OPB_ADD32 = 32, OPB_LNB16 = 64,
+  OPB_LNB32 = 128, OPB_DSILU = 256, OPS_ALL = 511,
+  OPS_EDGE_FWD = OPB_SILU | OPB_LNF16,
+  OPS_EDGE_BWD = OPB_SILU | OPB_LNB16 | OPB_DSILU | OPB_ADD16
+};
+__host__ __device__ inline int step_opbit(const Step& st) {
+  switch (st.epi) {
+    case EPI_SILU: return OPB_SILU;
+    case EPI_LN_FWD: return (st.flags & EF_RES16) ? OPB_LNF16 : OPB_LNF32;
+    case EPI_STORE: return OPB_STORE;
+    case EPI_ADD: return (st.flags & EF_G16) ? OPB_ADD16 : OPB_ADD32;
+    case EPI_LN_BWD: return (st.flags & EF_G16) ? OPB_LNB16 : OPB_LNB32;
+    case EPI_DSILU: return OPB_DSILU;
+    default: return OPS_ALL;
+  }
+}
+
 constexpr int MAX_STEPS = 8;
 constexpr int MAX_MAPS = 24;
 constexpr int NV_MAX = 5;  // column-sum vectors per kernel
@@ -356,7 +376,7 @@ namespace xmgn {
 //     written ACT half 0 and drained TMEM half 0, while half 1's epilogue still runs.
 // An A_TMA step stages its A chunk kc straight into ACT block kc (all K = H resident, read by
 // both N-halves).  LayerNorm steps still need both halves' row statistics (row_sum).
-template <int H, bool SPLIT, bool BWD, bool F16, bool Z1 = false, bool PIPE = false>
+template <int H, bool SPLIT, bool BWD, bool F16, bool Z1 = false, bool PIPE = false, int OPS = OPS_ALL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THREADS, 1)
     k_chain(const __grid_constant__ ChainParams p) {
   static_assert(!PIPE || (H == 512 && !SPLIT && !Z1 && EpiShape<SPLIT>::EW == 4), "PIPE: H = 512, 16-bit, 4 groups");
@@ -1058,32 +1078,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
           e.in_full = in_full; e.in_par = nin & 1; e.pol_last = pol_last;
           constexpr int NC16 = HC / 16;
           const int op = st.epi;
-          if (op == EPI_SILU) {
-            if constexpr (Z1) {
-              if (st.flags & EF_FROM_IN) op_silu_in<H, NC16, F16>(e, st, wait);
-              else op_silu<H, NC16, F16, false>(e, st, wait);
-            } else {
-              op_silu<H, NC16, F16, !BWD>(e, st, wait);
-            }
-            wrote_act = true;
-          } else if (op == EPI_LN_FWD) {
-            if (st.flags & EF_RES16) op_ln_fwd<H, NC16, F16, false>(e, st, wait, row_sum);
-            else op_ln_fwd<H, NC16, F16, true>(e, st, wait, row_sum);
-            wrote_act = (st.flags & EF_WRITE_ACT) != 0;
-          } else if (op == EPI_STORE) {
-            op_store<H, NC16, F16>(e, st, wait);
-          } else if (op == EPI_ADD) {
-            if (st.flags & EF_G16) op_add16<H, NC16, F16>(e, st, wait);
-            else op_add32<H, NC16, F16>(e, st, wait);
-          } else if constexpr (BWD) {
-            if (op == EPI_LN_BWD) {
-              if (st.flags & EF_G16) op_ln_bwd16<H, NC16, F16>(e, st, wait, row_sum);
-              else op_ln_bwd32<H, NC16, F16>(e, st, wait, row_sum);
+          const int ob = step_opbit(st);
+          if (ob == OPB_SILU) {
+            if constexpr ((OPS & OPB_SILU) != 0) {
+              if constexpr (Z1) {
+                if (st.flags & EF_FROM_IN) op_silu_in<H, NC16, F16>(e, st, wait);
+                else op_silu<H, NC16, F16, false>(e, st, wait);
+              } else {
+                op_silu<H, NC16, F16, !BWD>(e, st, wait);
+              }
               wrote_act = true;
-            } else if (op == EPI_DSILU) {
-              op_dsilu<H, NC16, F16>(e, st, wait);
-              wrote_act = !(st.flags & EF_NO_ACT);
             }
+          } else if (ob == OPB_LNF16) {
+            if constexpr ((OPS & OPB_LNF16) != 0) {
+              op_ln_fwd<H, NC16, F16, false>(e, st, wait, row_sum);
+              wrote_act = (st.flags & EF_WRITE_ACT) != 0;
+            }
+          } else if (ob == OPB_LNF32) {
+            if constexpr ((OPS & OPB_LNF32) != 0) {
+              op_ln_fwd<H, NC16, F16, true>(e, st, wait, row_sum);
+              wrote_act = (st.flags & EF_WRITE_ACT) != 0;
+            }
+          } else if (ob == OPB_STORE) {
+            if constexpr ((OPS & OPB_STORE) != 0) op_store<H, NC16, F16>(e, st, wait);
+          } else if (ob == OPB_ADD16) {
+            if constexpr ((OPS & OPB_ADD16) != 0) op_add16<H, NC16, F16>(e, st, wait);
+          } else if (ob == OPB_ADD32) {
+            if constexpr ((OPS & OPB_ADD32) != 0) op_add32<H, NC16, F16>(e, st, wait);
+          } else if constexpr (BWD) {
+            if (ob == OPB_LNB16) {
+              if constexpr ((OPS & OPB_LNB16) != 0) {
+                op_ln_bwd16<H, NC16, F16>(e, st, wait, row_sum);
+                wrote_act = true;
+              }
+            } else if (ob == OPB_LNB32) {
+              if constexpr ((OPS & OPB_LNB32) != 0) {
+                op_ln_bwd32<H, NC16, F16>(e, st, wait, row_sum);
+                wrote_act = true;
+              }
+            } else if (ob == OPB_DSILU) {
+              if constexpr ((OPS & OPB_DSILU) != 0) {
+                op_dsilu<H, NC16, F16>(e, st, wait);
+                wrote_act = !(st.flags & EF_NO_ACT);
+              }
+            }
+          }
+          if constexpr (OPS != OPS_ALL) {
+            if ((ob & OPS) == 0) __trap();   // the host picked a kernel without this op
           }
           // rows this step wrote with ordinary stores that a later step of this kernel reads
           // back by TMA (S' -> the dSiLU steps, G_e' -> the dX step): order the generic-proxy

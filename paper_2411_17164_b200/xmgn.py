@@ -84,6 +84,10 @@ _sig("xmgn_selftest_gemm", _i32, [_i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _
 _sig("xmgn_io_param_count", _sz, [ctypes.POINTER(ModelCfg)])
 _sig("xmgn_model_fwd", _i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp])
 _sig("xmgn_model_bwd", _i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp])
+_sig("xmgn_build_graph", _i32, [_vp, _i64, _vp, _i32, _i32, _i32, _i32, _i32, _vp, ctypes.POINTER(_vp)])
+_sig("xmgn_built_graph_desc", _i32, [_vp, ctypes.POINTER(GraphDesc)])
+_sig("xmgn_built_graph_owner", _i32, [_vp, _vp])
+_sig("xmgn_built_graph_free", None, [_vp])
 _sig("xmgn_launch_count", ctypes.c_longlong, [])
 _sig("xmgn_profile_enable", _i32, [_i32])
 _sig("xmgn_profile_collect", _i32, [ctypes.c_char_p, _sz, ctypes.POINTER(ctypes.c_double),
@@ -96,6 +100,7 @@ EXPORTS = ["xmgn_last_error", "xmgn_version", "xmgn_load_graph", "xmgn_part_info
            "xmgn_comm_unique_id", "xmgn_comm_init", "xmgn_grad_reduce", "xmgn_comm_destroy", "xmgn_gather_rows",
            "xmgn_scatter_rows",
            "xmgn_io_param_count", "xmgn_model_fwd", "xmgn_model_bwd",
+           "xmgn_build_graph", "xmgn_built_graph_desc", "xmgn_built_graph_owner", "xmgn_built_graph_free",
            "xmgn_cosine_lr", "xmgn_adam_step", "xmgn_selftest_gemm", "xmgn_launch_count", "xmgn_profile_enable", "xmgn_profile_collect"]
 
 
@@ -174,6 +179,40 @@ class Graph:
 
     def __del__(self):
         self.close()
+
+
+def build_graph(pos, level_counts, k, n_parts, halo_depth, stream=None):
+    """xmgn_build_graph (NEXT-4): the multi-scale kNN graph, RCB partitions and halo lists of a
+    device FP32 [n, 3] point cloud, returned as a bundle dict of numpy arrays (the layout of
+    xmgn_inputs.configs.build) -- every step runs on the GPU."""
+    n = int(pos.shape[0])
+    dv = pos.device.index
+    lc = _i64c(level_counts)
+    h = _vp()
+    _check(_lib.xmgn_build_graph(_dev_f32(pos, "pos", 3 * n), n, lc.ctypes.data, len(lc), int(k), int(n_parts),
+                                 int(halo_depth), dv, _stream(stream), ctypes.byref(h)))
+    try:
+        d = GraphDesc()
+        _check(_lib.xmgn_built_graph_desc(h, ctypes.byref(d)))
+        P = d.n_parts
+
+        def arr(ptr, count, dt):
+            if count == 0:
+                return np.zeros(0, dt)
+            ct = ctypes.c_int64 if dt == np.int64 else ctypes.c_int32
+            return np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ct)), shape=(count,)).astype(dt).copy()
+
+        oo = arr(d.owned_offsets, P + 1, np.int64)
+        ho = arr(d.halo_offsets, P + 1, np.int64)
+        out = dict(offsets=arr(d.csr_offsets, n + 1, np.int64), sources=arr(d.csr_sources, d.n_edges, np.int64),
+                   owned_offsets=oo, owned=arr(d.owned, int(oo[-1]), np.int64), halo_offsets=ho,
+                   halo=arr(d.halo, int(ho[-1]), np.int64), halo_ring=arr(d.halo_ring, int(ho[-1]), np.int32))
+        owner = np.empty(n, np.int64)
+        _check(_lib.xmgn_built_graph_owner(h, owner.ctypes.data))
+        out["owner"] = owner
+        return out
+    finally:
+        _lib.xmgn_built_graph_free(h)
 
 
 def model_cfg(hidden, layers, m=2, precision=PREC_FP16, ln_eps=1e-5):
