@@ -16,7 +16,7 @@
 
 // dgamma column sums of the LN backward: deferred read-modify-writes (1) or one per chunk (0)
 #ifndef XMGN_DEFER_DGAMMA
-#define XMGN_DEFER_DGAMMA 1
+#define XMGN_DEFER_DGAMMA 0
 #endif
 
 namespace xmgn {
@@ -104,6 +104,14 @@ __device__ __forceinline__ void sts_tile16(uint8_t* tile, int row, int c0, const
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a1), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7])
                : "memory");
 }
+// the same from already packed 16-bit words
+__device__ __forceinline__ void sts_tile16_packed(uint8_t* tile, int row, int c0, const uint32_t* h) {
+  const uint32_t a0 = tile_addr16(tile, row, c0), a1 = tile_addr16(tile, row, c0 + 8);
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a0), "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3])
+               : "memory");
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a1), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7])
+               : "memory");
+}
 template <bool F16>
 __device__ __forceinline__ void lds_tile16(uint8_t* tile, int row, int c0, float* v) {
   uint32_t h[8];
@@ -177,8 +185,10 @@ struct Epi {
 
 // 16 values of this row's TMA-loaded input (ACT, columns c0 .. c0+15), after the box landed
 template <bool F16>
+// (chunks are consumed in increasing column order: the box's barrier is waited on at the box's
+// first chunk, or at this thread's first chunk when it starts inside a box)
 __device__ __forceinline__ void in16(const Epi& e, int c0, float* v) {
-  mbar_wait(&e.in_full[c0 >> 6], e.in_par);
+  if ((c0 & 63) == 0 || c0 == e.cb) mbar_wait(&e.in_full[c0 >> 6], e.in_par);
   lds_tile16<F16>(e.act, e.trow, c0, v);
 }
 
@@ -452,9 +462,13 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
       if (has_g && !tin) ld16(gp16 + (cc + 2) * 16, gq);
       if (ga) ld16(ap16 + (cc + 2) * 16, aq);
     }
-    round16<F16>(dy);                                // as stored (G_e')
-    if (ga) st16<F16>(gp16 + cc * 16, dy);
-    sts_tile16<F16>(e.act, e.trow, c0, dy);          // stash for pass B
+    {                                                // dy <- dy as stored (G_e'), packed once
+      uint32_t h[8];
+      pack16x16<F16>(dy, h);
+      cvt16<F16>(h, dy);
+      if (ga) stg256(gp16 + cc * 16, h);
+      sts_tile16_packed(e.act, e.trow, c0, h);       // stash for pass B
+    }
     lds16(e.sb + cc * 16, xh);
     tmem_wait16(ta);
 #pragma unroll
