@@ -141,6 +141,9 @@ constexpr int NV_MAX = 5;  // column-sum vectors per kernel
 // rows (row statistics are exchanged through shared memory).  The 16-bit modes
 // use four column groups (16 epilogue warps, latency tolerance); the FP32 check
 // mode keeps two (its hi/lo operands need the registers).
+#ifndef XMGN_CTRL_REGS
+#define XMGN_CTRL_REGS 56
+#endif
 #ifndef XMGN_EPI_GROUPS
 #define XMGN_EPI_GROUPS 4
 #endif
@@ -152,7 +155,7 @@ struct EpiShape {
   // count ptxas derives from __launch_bounds__); setmaxnreg.inc can only take what
   // the control warpgroup released with setmaxnreg.dec, or it blocks forever.
   static constexpr int LAUNCH_REGS = (65536 / THREADS) & ~7;
-  static constexpr int CTRL_REGS = 56;
+  static constexpr int CTRL_REGS = XMGN_CTRL_REGS;   // control warps after setmaxnreg.dec
   static constexpr int EPI_REGS_FIT = (LAUNCH_REGS + (LAUNCH_REGS - CTRL_REGS) / EW) & ~7;
   static constexpr int EPI_REGS = EPI_REGS_FIT > 224 ? 224 : EPI_REGS_FIT;
   static_assert(128 * CTRL_REGS + 128 * EW * EPI_REGS <= THREADS * LAUNCH_REGS, "register pool");
@@ -165,9 +168,13 @@ struct ChainParams {
   int M;              // rows
   const int* src;     // [M] source local id of each edge row (edge programs)
   const int* dst;     // [M] destination local id
-  float* colsum;      // [gridDim.x][4][NV_MAX][H] partial column sums (backward)
+  float* colsum;      // partial column sums (backward): [slot][CTA tile 2 t + rank][quadrant][H]
+  long long cs_vstride;   // elements per slot (= CTA tiles x 4 x H)
+  int cs_slot[NV_MAX];    // column-sum vector -> slot (-1: the program never writes it)
   float eps;          // LayerNorm epsilon
+  int* tile_counter;  // dynamic tile scheduler: zeroed before the launch (null = static tiles)
 };
+constexpr int TQ = 2;   // tile-queue slots per cluster (the producer claims at most one tile ahead)
 
 template <int H, bool SPLIT>
 struct ChainCfg {
@@ -362,6 +369,45 @@ __device__ __forceinline__ void load_dy(const Step& st, bool has_g, bool valid, 
 #include "epi16.cuh"
 namespace xmgn {
 
+// Tile schedule of the chain kernel (see k_chain): static, or dynamic through a queue the
+// leader's producer fills from an atomic counter.
+// The dynamic queue is compiled out by default: on B200 its extra live state made the epilogue
+// spill (edge bwd +5%, profiles/r02d_ab_tiles.jsonl), more than the end-of-kernel tail it removes.
+// Build with -DXMGN_STATIC_TILES=0 and run with XMGN_DYN=1 to use it.
+#ifndef XMGN_STATIC_TILES
+#define XMGN_STATIC_TILES 1
+#endif
+struct TileSched {   // everything but the queue base is re-derived at each call (few live registers)
+  const ChainParams* p;
+  uint64_t* base;        // tq_full[TQ], tq_empty[TQ], then int q[TQ]
+  __device__ __forceinline__ int at(int i) const {   // every role
+    if (XMGN_STATIC_TILES || !p->tile_counter) {
+      const int t = (int)cluster_id_x() + i * (int)n_clusters_x();
+      return t < (p->M + 255) / 256 ? t : -1;
+    }
+    mbar_wait_cluster(&base[i % TQ], (i / TQ) & 1);
+    return *reinterpret_cast<volatile int*>(reinterpret_cast<int*>(base + 2 * TQ) + i % TQ);
+  }
+  __device__ __forceinline__ int claim(int i) const {   // the leader's producer (one lane)
+    if (XMGN_STATIC_TILES || !p->tile_counter) return at(i);
+    const int slot = i % TQ;
+    if (i >= TQ) mbar_wait_cluster(&base[TQ + slot], ((i / TQ) - 1) & 1);
+    const int t = atomicAdd(p->tile_counter, 1);
+    const int tile = t < (p->M + 255) / 256 ? t : -1;
+    int* q = reinterpret_cast<int*>(base + 2 * TQ) + slot;
+    *q = tile;
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(mapa_shared(smem_u32(q), 1)), "r"(tile) : "memory");
+    mbar_arrive(&base[slot]);
+    mbar_arrive_cluster(mapa_shared(smem_u32(&base[slot]), 1));
+    return tile;
+  }
+  __device__ __forceinline__ void done(int i) const {   // hand-off warps, lane 0, after the tile
+    if (XMGN_STATIC_TILES || !p->tile_counter) return;
+    if (cluster_ctarank() == 0) mbar_arrive(&base[TQ + i % TQ]);
+    else mbar_arrive_cluster(mapa_shared(smem_u32(&base[TQ + i % TQ]), 0));
+  }
+};
+
 // Z1: backward programs whose first edge step reloads the forward's z_1 checkpoint
 // (a separate instantiation so the regular backward kernel's register allocation is
 // unaffected)
@@ -409,7 +455,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
   uint64_t* act_full2 = acc_empty2 + 2;      // [2] epilogue half h (both CTAs) -> MMA (ACT half written)
   uint64_t* act_rd = act_full2 + 2;          // [2] MMA -> epilogue / producer: ACT half no longer read
   uint64_t* act_idle = act_rd + 2;           // [2] local epilogue half -> local producer: ACT half idle
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(act_idle + 2);
+  uint64_t* tq_full = act_idle + 2;          // [TQ] tile-queue entry written (both CTAs)
+  uint64_t* tq_empty = tq_full + TQ;         // [TQ] leader: entry consumed by every role of both CTAs
+  int* tq = reinterpret_cast<int*>(tq_empty + TQ);   // [TQ] queued pair-tile ids (-1: no more)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tq + TQ);
+  static_assert(8 * (2 * C::SA + 2 * C::SB + 5 + H / 64 + 10 + 2 * TQ) + 4 * TQ + 4 <= 512,
+                "barrier region overflows RED_OFF");
   float* red = reinterpret_cast<float*>(smem + C::RED_OFF);
   float* prm_base = reinterpret_cast<float*>(smem + C::PRM_OFF);
 
@@ -427,6 +478,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
     mbar_init(act_free, 1);
     mbar_init(mma_idle, 1);
     for (int i = 0; i < H / 64; ++i) mbar_init(&in_full[i], 1);
+    for (int i = 0; i < TQ; ++i) {
+      mbar_init(&tq_full[i], 1);
+      mbar_init(&tq_empty[i], 2 * (PIPE ? 2 : 1));   // the hand-off warps of both CTAs
+    }
     if constexpr (PIPE) {
       for (int h = 0; h < 2; ++h) {
         mbar_init(&acc_full2[h], 1);
@@ -447,6 +502,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
+  // ---- tile schedule.  Static: cluster cid takes tiles cid, cid + ncl, ...  Dynamic (tile_counter):
+  // the leader's producer claims pair tiles with an atomic counter and queues them in both
+  // CTAs' tq[] (TQ slots); every role reads the same sequence.  A slot is reused only after the
+  // hand-off warps of both CTAs finished its tile, by which time every role has read it.
+  const TileSched ts{&p, tq_full};
+
   // register split (setmaxnreg, per warpgroup): control warps 0-3 need few registers,
   // the epilogue warpgroups get the rest
   if (w < 4) {
@@ -456,7 +517,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
     // A_TMA chunk kc -> ACT block kc once the previous step is done with that ACT half
     if (elect_one()) {
       int bi = 0, g = 0;
-      for (int tile = cid; tile < n_tiles; tile += ncl) {
+      int nid0 = 0, nid1 = 0;   // act_idle waits per ACT half (each matched by one hand-off arrive)
+      for (int it = 0, tile; (tile = rank == 0 ? ts.claim(it) : ts.at(it)) >= 0; ++it) {
         const int row0 = tile * 256 + (int)rank * 128;
         for (int s = 0; s < p.n_steps; ++s, ++g) {
           const Step& st = p.steps[s];
@@ -471,7 +533,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
                   // the previous step's epilogue used it (skipped when that epilogue never touches
                   // ACT: the A loads then overlap it)
                   const Step& pv = p.steps[s > 0 ? s - 1 : p.n_steps - 1];
-                  if (step_uses_act(pv)) mbar_wait(&act_idle[kh], (g - 1) & 1);
+                  if (step_uses_act(pv)) {
+                    if (kh == 0) mbar_wait(&act_idle[0], nid0++ & 1);
+                    else mbar_wait(&act_idle[1], nid1++ & 1);
+                  }
                 }
                 if (rank == 0) mbar_expect_tx(&a_full[kc], 2 * C::A_SLOT);
                 const uint32_t fb = mapa_shared(smem_u32(&a_full[kc]), 0);
@@ -499,7 +564,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
       constexpr uint32_t idesc = idesc_pair(NB, F16);
       constexpr int NK = H / 64;
       int bi = 0, g = 0, na = 0;
-      for (int tile = cid; tile < n_tiles; tile += ncl) {
+      for (int it = 0, tile; (tile = ts.at(it)) >= 0; ++it) {
         for (int s = 0; s < p.n_steps; ++s, ++g) {
           const Step& st = p.steps[s];
           const bool tma_a = st.a_src == A_TMA;
@@ -541,7 +606,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
     // ============================ TMA producer (both CTAs: own A rows, own half of B)
     if (elect_one()) {
       int ai = 0, bi = 0, g = 0, naf = 0;  // A / B ring fills, global step, act_free phases
-      for (int tile = cid; tile < n_tiles; tile += ncl) {
+      for (int it = 0, tile; (tile = rank == 0 ? ts.claim(it) : ts.at(it)) >= 0; ++it) {
         const int row0 = tile * 256 + (int)rank * 128;
         for (int s = 0; s < p.n_steps; ++s, ++g) {
           const Step& st = p.steps[s];
@@ -582,7 +647,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
       constexpr uint32_t idesc = idesc_pair(NB, F16);
       const uint32_t act_free_peer = mapa_shared(smem_u32(act_free), 1);
       int ai = 0, bi = 0, g = 0, nact = 0, nidle = 0;
-      for (int tile = cid; tile < n_tiles; tile += ncl) {
+      for (int it = 0, tile; (tile = ts.at(it)) >= 0; ++it) {
         for (int s = 0; s < p.n_steps; ++s, ++g) {
           const Step& st = p.steps[s];
           const bool tma_a = st.a_src == A_TMA;
@@ -655,13 +720,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
     const int h = w == 3 ? 0 : 1;
     const uint32_t ae_l = mapa_shared(smem_u32(&acc_empty2[h]), 0);
     const uint32_t af_l = mapa_shared(smem_u32(&act_full2[h]), 0);
-    for (int tile = cid; tile < n_tiles; tile += ncl) {
+    for (int it = 0, tile; (tile = ts.at(it)) >= 0; ++it) {
       for (int s = 0; s < p.n_steps; ++s) {
         named_bar(7 + h, 256 + 32);
         if (lane_id() == 0) {
-          // act_idle first: once the MMA has seen this step's acc_empty, act_idle has completed
-          // this step's phase too, so the producer's parity waits never see it two phases behind
-          mbar_arrive(&act_idle[h]);
+          // act_idle only when the producer will wait for it (the next step stages its A by TMA
+          // into ACT and this step used ACT): every phase is waited on, and it is arrived first so
+          // it has completed by the time the MMA sees this step's acc_empty
+          if (p.steps[s + 1 < p.n_steps ? s + 1 : 0].a_src == A_TMA && step_uses_act(p.steps[s]))
+            mbar_arrive(&act_idle[h]);
           if (rank == 0) {
             mbar_arrive(&acc_empty2[h]);
             mbar_arrive(&act_full2[h]);
@@ -672,6 +739,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         }
         __syncwarp();
       }
+      if (lane_id() == 0) ts.done(it);
+      __syncwarp();
     }
   } else if (w == 3) {
     // ============================ step hand-off: joins the epilogue's end-of-step barrier and
@@ -681,7 +750,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
     const uint32_t acc_empty_l = mapa_shared(smem_u32(acc_empty), 0);
     const uint32_t act_full_l = mapa_shared(smem_u32(act_full), 0);
     int g = 0;
-    for (int tile = cid; tile < n_tiles; tile += ncl) {
+    for (int it = 0, tile; (tile = ts.at(it)) >= 0; ++it) {
       for (int s = 0; s < p.n_steps; ++s, ++g) {
         const Step& st = p.steps[s];
         const bool wa = step_writes_act(st);
@@ -697,6 +766,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         }
         __syncwarp();
       }
+      if (lane_id() == 0) ts.done(it);
+      __syncwarp();
     }
   }
   } else {
@@ -723,14 +794,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         return t;
       }
     };
-    // per-(CTA, quadrant) column-sum partials live in global memory (zeroed by the
-    // host); lane l of this warp owns column c0 + l of every chunk, so the
-    // read-modify-write below is race-free and runs in a fixed order.
-    float* colsum_base = p.colsum ? p.colsum + ((size_t)blockIdx.x * 4 + q) * NV_MAX * H : nullptr;
+    // per-(CTA tile, quadrant) column-sum partials in global memory: lane l of this warp owns
+    // column c0 + l of every chunk; each entry is written exactly once per launch (by the one
+    // warp that runs that tile and quadrant), so the partials do not depend on the CTA <-> tile
+    // assignment and k_reduce_colsum sums them in a fixed order.
+    float* colsum_base = nullptr;
     auto colsum_add = [&](int vec, int c0, float* vals) {
       const float cs = warp_colsum32(vals);
-      float* dstp = colsum_base + (size_t)vec * H + c0 + lane;
-      *dstp += cs;
+      colsum_base[(size_t)p.cs_slot[vec] * p.cs_vstride + c0 + lane] = cs;
     };
     int g = 0, nin = 0;   // nin: steps whose input came through in_full (its phase)
     const uint64_t pol_last = policy_evict_last();
@@ -742,12 +813,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
     constexpr int SBAR_THREADS = GROUP_STORES ? 128 : NEPI;
     const bool issuer = GROUP_STORES ? (q == 0 && lane == 0) : (threadIdx.x == 128);
     bool st_pending = false;   // TMA stores out of ACT may still be reading it
-    for (int tile = cid; tile < n_tiles; tile += ncl) {
+    for (int it = 0, tile; (tile = ts.at(it)) >= 0; ++it) {
       const int r = tile * 256 + (int)rank * 128 + trow;
       const bool valid = r < p.M;
       const int rr = valid ? r : 0;
       const int src = p.src ? p.src[rr] : 0;
       const int dst = p.dst ? p.dst[rr] : 0;
+      colsum_base = p.colsum ? p.colsum + ((size_t)(2 * tile + (int)rank) * 4 + q) * H : nullptr;
       for (int s = 0; s < p.n_steps; ++s, ++g) {
         const Step& st = p.steps[s];
         float* prm = prm_base + (g & 1) * 3 * H;
@@ -1074,7 +1146,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
           };
           Epi e;
           e.act = act; e.tl = tl; e.trow = trow; e.cb = cb; e.r = r; e.src = src; e.dst = dst; e.valid = valid;
-          e.sb = prm + cb; e.sg = prm + H + cb; e.sbt = prm + 2 * H + cb; e.colsum = colsum_base; e.eps = p.eps;
+          e.sb = prm + cb; e.sg = prm + H + cb; e.sbt = prm + 2 * H + cb; e.colsum = colsum_base; e.cs_vstride = (size_t)p.cs_vstride; e.cs_slot = p.cs_slot; e.eps = p.eps;
           e.in_full = in_full; e.in_par = nin & 1; e.pol_last = pol_last;
           constexpr int NC16 = HC / 16;
           const int op = st.epi;

@@ -14,10 +14,6 @@
 #pragma once
 #include "tc.cuh"
 
-// dgamma column sums of the LN backward: deferred read-modify-writes (1) or one per chunk (0)
-#ifndef XMGN_DEFER_DGAMMA
-#define XMGN_DEFER_DGAMMA 0
-#endif
 
 namespace xmgn {
 
@@ -176,7 +172,9 @@ struct Epi {
   const float* sb;   // bias  [cb ..] in shared memory
   const float* sg;   // gamma [cb ..]
   const float* sbt;  // beta  [cb ..]
-  float* colsum;     // per-(CTA, quadrant) column-sum partials [NV_MAX][H] (backward)
+  float* colsum;     // this (CTA tile, quadrant)'s column-sum partials, vector slot stride cs_vstride
+  size_t cs_vstride;
+  const int* cs_slot;  // vector -> slot of the partial buffer
   float eps;
   uint64_t* in_full; // [H/64] mbarriers: TMA-loaded input boxes in ACT (Step::in_map)
   uint32_t in_par;   // their phase parity for this step
@@ -192,31 +190,14 @@ __device__ __forceinline__ void in16(const Epi& e, int c0, float* v) {
   lds_tile16<F16>(e.act, e.trow, c0, v);
 }
 
-// Deferred form for the per-chunk dgamma sums: the warp sum of chunk cc is kept in
-// acc[cc] (lanes 0-15 hold column c0 + lane) and colsum16_flush issues all NC read-modify-
-// writes back to back (one exposed global latency per step instead of NC).
-template <int NC>
-__device__ __forceinline__ void colsum16_flush(const Epi& e, int vec, const float* acc) {
-  constexpr int HT = NC * 16 * 4;   // H (4 column groups of NC x 16)
-  const int lane = lane_id();
-  if (lane < 16) {
-    float* d = e.colsum + (size_t)vec * HT + e.cb + lane;
-    float old[NC];
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc) old[cc] = d[cc * 16];
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc) d[cc * 16] = old[cc] + acc[cc];
-  }
-}
-
+// Column sums of this warp's 32 rows for columns c0 .. c0+15 -> this tile's partial of vector
+// `vec` (written once: every (tile, quadrant, column) has exactly one writer, so no
+// read-modify-write and no dependence on which CTA runs the tile)
 template <int H>
 __device__ __forceinline__ void colsum16_add(const Epi& e, int vec, int c0, float* vals) {
   const float cs = warp_colsum16(vals);
   const int lane = lane_id();
-  if (lane < 16) {
-    float* d = e.colsum + (size_t)vec * H + c0 + lane;
-    *d += cs;
-  }
+  if (lane < 16) e.colsum[(size_t)e.cs_slot[vec] * e.cs_vstride + c0 + lane] = cs;
 }
 
 // Row statistics (mean, rstd) of z = acc + b over the H columns of this row, in
@@ -427,6 +408,9 @@ __device__ __forceinline__ void op_ln_fwd(const Epi& e, const Step& st, Wait wai
   }
 }
 
+// Both LN backward forms rely on dY = 0 on rows >= M (TMA out-of-bounds fill, unloaded
+// registers, no G_a gather): every product with dY then vanishes there (x^ is finite: those
+// rows' accumulators are finite), so no per-element row mask is needed.
 // EPI_LN_BWD, edge form (EF_G16): dY = G_e (rows < valid_in) + G_a[dst], written
 // back (16-bit) as G_e'; LayerNorm backward dz = rstd (dY*g - mean(dY*g) - x^ mean(dY*g x^))
 // -> ACT + scratch dZ; dgamma (and with EF_COLSUM_ALL dbeta, db) column sums.
@@ -449,7 +433,6 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
   float mean, rstd;
   ln_stats16<H, NC>(e, e.eps, row_sum, mean, rstd);
   float s1 = 0.f, s2 = 0.f;
-  float dg[NC];   // deferred dgamma warp sums (colsum16_flush)
   uint32_t ta[16];
   tmem_ld16_async(e.tl, ta);
   auto passA = [&](int cc, uint32_t* gq, uint32_t* aq) {
@@ -481,34 +464,20 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
       const float dxh = dy[i] * gm[i];
       s1 += dxh;
       s2 += dxh * xh[i];
-      gm[i] = e.valid ? dy[i] * xh[i] : 0.f;       // dgamma terms
+      gm[i] = dy[i] * xh[i];                       // dgamma terms (dy = 0 on rows >= M)
     }
-#if XMGN_DEFER_DGAMMA
-    dg[cc] = warp_colsum16(gm);
-#else
     colsum16_add<H>(e, 0, c0, gm);
-#endif
     if (csall) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) xh[i] = e.valid ? dy[i] : 0.f;
+      for (int i = 0; i < 16; ++i) xh[i] = dy[i];
       colsum16_add<H>(e, 1, c0, xh);                 // dbeta
     }
   };
-#if XMGN_DEFER_DGAMMA
-#pragma unroll
-  for (int cc = 0; cc < NC; cc += 2) {
-    passA(cc, g0, a0);
-    passA(cc + 1, g1, a1);
-  }
-  colsum16_flush<NC>(e, 0, dg);
-#else
-  (void)dg;
 #pragma unroll 1
   for (int cc = 0; cc < NC; cc += 2) {
     passA(cc, g0, a0);
     passA(cc + 1, g1, a1);
   }
-#endif
   s1 = row_sum(s1) * (1.0f / H);
   s2 = row_sum(s2) * (1.0f / H);
   tmem_ld16_async(e.tl, ta);
@@ -525,7 +494,7 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
     float gm[16];
     lds16(e.sg + cc * 16, gm);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) dy[i] = e.valid ? rstd * (dy[i] * gm[i] - s1 - xh[i] * s2) : 0.f;
+    for (int i = 0; i < 16; ++i) dy[i] = rstd * (dy[i] * gm[i] - s1 - xh[i] * s2);
     sts_tile16<F16>(e.act, e.trow, c0, dy);
     if (e.valid && st.st_map < 0) st16<F16>(zp + cc * 16, dy);
     if (csall) colsum16_add<H>(e, 2, c0, dy);        // db_{m+1}
@@ -567,12 +536,12 @@ __device__ __forceinline__ void op_ln_bwd32(const Epi& e, const Step& st, Wait w
       const float dxh = dy[i] * gm[i];
       s1 += dxh;
       s2 += dxh * xh[i];
-      gm[i] = e.valid ? dy[i] * xh[i] : 0.f;
+      gm[i] = dy[i] * xh[i];
     }
     colsum16_add<H>(e, 0, c0, gm);
     if (csall) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) xh[i] = e.valid ? dy[i] : 0.f;
+      for (int i = 0; i < 16; ++i) xh[i] = dy[i];
       colsum16_add<H>(e, 1, c0, xh);
     }
   };
@@ -599,7 +568,7 @@ __device__ __forceinline__ void op_ln_bwd32(const Epi& e, const Step& st, Wait w
     float gm[16];
     lds16(e.sg + cc * 16, gm);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) dy[i] = e.valid ? rstd * (dy[i] * gm[i] - s1 - xh[i] * s2) : 0.f;
+    for (int i = 0; i < 16; ++i) dy[i] = rstd * (dy[i] * gm[i] - s1 - xh[i] * s2);
     sts_tile16<F16>(e.act, e.trow, c0, dy);
     if (e.valid && st.st_map < 0) st16<F16>(zp + cc * 16, dy);
     if (csall) colsum16_add<H>(e, 2, c0, dy);

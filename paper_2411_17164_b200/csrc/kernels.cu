@@ -464,15 +464,30 @@ __global__ void k_reduce_part(const float* __restrict__ part, int S, long long n
   }
 }
 
-// Column-sum partials [nblk][4][NV][H] -> grad[dst[v] + c] += sum (fixed order).
-__global__ void k_reduce_colsum(const float* __restrict__ part, int nblk, int nv, int H, ColsumDst dsts,
-                                float* __restrict__ grad, const float* __restrict__ inv) {
+// Column-sum partials [slot][CTA tile][quadrant][H] -> grad[dst[v] + c] += inv * sum, in two
+// fixed-order levels: CS_SEG contiguous tile segments, then the segments in order.
+struct CsSlots {
+  int s[NV_COLSUM];
+};
+__global__ void k_colsum_seg(const float* __restrict__ part, int nct, CsSlots slot, ColsumDst dsts, int H,
+                             float* __restrict__ tmp) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x, seg = blockIdx.y, v = blockIdx.z;
+  if (c >= H || dsts.off[v] < 0) return;
+  const long long vs = (long long)nct * 4 * H;
+  const float* pv = part + (long long)slot.s[v] * vs;
+  const int t0 = (int)((long long)nct * seg / CS_SEG), t1 = (int)((long long)nct * (seg + 1) / CS_SEG);
+  float s = 0.f;
+  for (long long r = (long long)t0 * 4; r < (long long)t1 * 4; ++r) s += pv[r * H + c];
+  tmp[((size_t)v * CS_SEG + seg) * H + c] = s;
+}
+__global__ void k_colsum_fin(const float* __restrict__ tmp, ColsumDst dsts, int H, float* __restrict__ grad,
+                             const float* __restrict__ inv) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nv * H) return;
+  if (t >= NV_COLSUM * H) return;
   const int v = t / H, c = t % H;
   if (dsts.off[v] < 0) return;
   float s = 0.f;
-  for (int b = 0; b < nblk * 4; ++b) s += part[((size_t)b * NV_COLSUM + v) * H + c];
+  for (int g = 0; g < CS_SEG; ++g) s += tmp[((size_t)v * CS_SEG + g) * H + c];
   grad[dsts.off[v] + c] += s * (inv ? *inv : 1.0f);
 }
 
@@ -638,10 +653,13 @@ void launch_reduce_part(const float* part, int S, long long n, long long ld, flo
   int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
   k_reduce_part<<<blocks, 256, 0, st>>>(part, S, n, ld, grad, inv);
 }
-void launch_reduce_colsum(const float* part, int nblk, int nv, int H, ColsumDst d, float* grad, cudaStream_t st,
-                          const float* inv) {
-  count_launch();
-  k_reduce_colsum<<<(nv * H + 255) / 256, 256, 0, st>>>(part, nblk, nv, H, d, grad, inv);
+void launch_reduce_colsum(const float* part, int nct, const int* slot, int H, ColsumDst d, float* tmp, float* grad,
+                          cudaStream_t st, const float* inv) {
+  count_launch(2);
+  CsSlots sl;
+  for (int v = 0; v < NV_COLSUM; ++v) sl.s[v] = slot[v] < 0 ? 0 : slot[v];
+  k_colsum_seg<<<dim3((H + 127) / 128, CS_SEG, NV_COLSUM), 128, 0, st>>>(part, nct, sl, d, H, tmp);
+  k_colsum_fin<<<(NV_COLSUM * H + 255) / 256, 256, 0, st>>>(tmp, d, H, grad, inv);
 }
 void launch_scatter_rows(const float* src, const long long* idx, long long n, long long row_elems, float* dst,
                          cudaStream_t st) {

@@ -65,7 +65,11 @@ struct xmgn_workspace {
   xmgn::BfBuf scrA[2], scrS[2], scrZ[3], D;
   float* part = nullptr;  // wgrad split-K partials
   int part_splits = 0;
-  float* colsum = nullptr;
+  float* colsum = nullptr;        // per-tile column-sum partials (chain.cuh), colsum_cap floats
+  size_t colsum_cap = 0;
+  float* cs_tmp = nullptr;        // [NV_MAX][CS_SEG][H] first-level sums of the colsum reduce
+  int cs_slot[xmgn::NV_MAX];      // slot map of the last backward chain launch
+  int cs_nct = 0;                 // its CTA tiles
   unsigned int* d_amax = nullptr;  // max|g| bits of the current backward's seed
   float* d_scale = nullptr;        // {S, 1/S}: the backward's power-of-two loss scale
   int last_fwd = -1;
@@ -90,6 +94,8 @@ struct xmgn_workspace {
   int head_warps = 0;
   bool infer = false;   // inference workspace: forward only, per-layer buffers ping-ponged
   bool pipe = true;     // N-half-pipelined chain kernel where a program allows it (XMGN_PIPE=0: off)
+  bool dyn = false;     // dynamic tile scheduling in the chain kernels (XMGN_DYN=1, needs XMGN_STATIC_TILES=0)
+  int* d_tile_counter = nullptr;
   // checkpoint slot of layer l's tensors (training: one per layer; inference: ping-pong)
   long long ck(int l) const { return infer ? (l & 1) : l; }
 };
@@ -254,9 +260,31 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
   const int pair_tiles = (M + 255) / 256;
   const int grid = 2 * (pair_tiles < ws->sms / 2 ? pair_tiles : ws->sms / 2);
   p.colsum = bwd ? ws->colsum : nullptr;
-  if (bwd)
-    XMGN_CUDA(cudaMemsetAsync(ws->colsum, 0, (size_t)grid * 4 * NV_MAX * ws->H * sizeof(float), st), "colsum zero");
+  if (bwd) {
+    // column-sum vectors this program writes -> consecutive slots of per-tile partials (each
+    // written once per launch: no zeroing)
+    bool used[NV_MAX] = {false, false, false, false, false};
+    for (int s = 0; s < n; ++s) {
+      const Step& S = p.steps[s];
+      if (S.epi == EPI_LN_BWD) {
+        used[0] = true;
+        if (S.flags & EF_COLSUM_ALL) used[1] = used[2] = true;
+      }
+      if (S.epi == EPI_DSILU && (S.flags & EF_COLSUM_ALL)) used[S.vec0] = true;
+    }
+    int ns = 0;
+    for (int v = 0; v < NV_MAX; ++v) p.cs_slot[v] = used[v] ? ns++ : -1;
+    const int nct = 2 * pair_tiles;
+    p.cs_vstride = (long long)nct * 4 * ws->H;
+    if ((size_t)ns * (size_t)p.cs_vstride > ws->colsum_cap)
+      throw Fail{set_error(XMGN_ESTATE, "internal: column-sum partials exceed the workspace (%d slots x %d tiles)", ns,
+                           nct)};
+    for (int v = 0; v < NV_MAX; ++v) ws->cs_slot[v] = p.cs_slot[v];
+    ws->cs_nct = nct;
+  }
   const bool pipe = ws->pipe && chain_can_pipe(ws->H, ws->split, p);
+  p.tile_counter = ws->dyn ? ws->d_tile_counter : nullptr;
+  if (ws->dyn) XMGN_CUDA(cudaMemsetAsync(ws->d_tile_counter, 0, sizeof(int), st), "tile counter");
   {
     ProfScope ps(name, st);
     launch_chain(ws->H, ws->split, ws->f16, bwd, p, grid, st, pipe);
@@ -323,8 +351,18 @@ static void wgrad(xmgn_workspace* ws, const BfBuf& a0, const BfBuf& a1, int a_wi
   if (p.ones_tile) launch_reduce_part(ws->part + (long long)Hin * H, S, H, ld, grad + bias_dst, st, inv);
 }
 
+// grad[off[v] + c] += (1/S) sum over the last backward launch's tiles and quadrants of vector v
+static void reduce_colsums(xmgn_workspace* ws, const ColsumDst& d, float* grad, cudaStream_t st) {
+  ColsumDst dd = d;
+  for (int v = 0; v < NV_MAX; ++v)
+    if (dd.off[v] >= 0 && ws->cs_slot[v] < 0)
+      throw Fail{set_error(XMGN_ESTATE, "internal: column-sum vector %d was not written", v)};
+  launch_reduce_colsum(ws->colsum, ws->cs_nct, ws->cs_slot, ws->H, dd, ws->cs_tmp, grad, st, ws->d_scale + 1);
+}
+
 static void colsum_reduce(xmgn_workspace* ws, int blk, int l, float* grad, int grid_used, cudaStream_t st,
                           bool gamma_only = false) {
+  (void)grid_used;
   Layout Ly{ws->H, ws->L, ws->m};
   ColsumDst d;
   for (int v = 0; v < NV_MAX; ++v) d.off[v] = -1;
@@ -335,7 +373,7 @@ static void colsum_reduce(xmgn_workspace* ws, int blk, int l, float* grad, int g
     d.off[3] = Ly.b(l, blk, ws->m - 1);
     if (ws->m >= 2) d.off[4] = Ly.b(l, blk, ws->m - 2);
   }
-  launch_reduce_colsum(ws->colsum, grid_used, NV_MAX, ws->H, d, grad, st, ws->d_scale + 1);
+  reduce_colsums(ws, d, grad, st);
 }
 
 }  // namespace xmgn
@@ -375,6 +413,7 @@ static xmgn_status workspace_create(const xmgn_graph* g, const xmgn_model_cfg* c
       ws->cfg = *cfg;
       ws->infer = infer;
       { const char* pe = getenv("XMGN_PIPE"); ws->pipe = !(pe && atoi(pe) == 0); }
+      { const char* de = getenv("XMGN_DYN"); ws->dyn = de && atoi(de) == 1; }   // see XMGN_STATIC_TILES
       ws->dev = g->device;
       ws->H = H; ws->L = L; ws->m = m;
       ws->split = cfg->precision == XMGN_PREC_FP32_CHECK;
@@ -432,9 +471,14 @@ static xmgn_status workspace_create(const xmgn_graph* g, const xmgn_model_cfg* c
         ws->D = bfalloc(ws, 2 * NH);
         ws->part_splits = 64;
         ws->part = (float*)dalloc(ws, (size_t)ws->part_splits * (2 * H + 128) * H * 4);
-        ws->colsum = (float*)dalloc(ws, (size_t)ws->sms * 4 * NV_MAX * H * 4);
+        // per-tile partials: edge programs write one vector (dgamma), node programs up to NV_MAX
+        const size_t nct_e = 2 * (size_t)((ws->Emax + 255) / 256), nct_n = 2 * (size_t)((ws->Nmax + 255) / 256);
+        ws->colsum_cap = std::max(nct_e, NV_MAX * nct_n) * 4 * H;
+        ws->colsum = (float*)dalloc(ws, ws->colsum_cap * 4);
+        ws->cs_tmp = (float*)dalloc(ws, (size_t)NV_MAX * CS_SEG * H * 4);
       }
       ws->d_amax = (unsigned int*)dalloc(ws, 4);
+      ws->d_tile_counter = (int*)dalloc(ws, 4);
       ws->d_scale = (float*)dalloc(ws, 2 * sizeof(float));
       // Opt-in (XMGN_Z1=1) memory-for-speed mode: z_1 checkpoints (+L x E x H x 2 bytes) let
       // the backward skip the first edge GEMM's recompute (edge bwd -5%).  Off by default: at
@@ -892,7 +936,7 @@ static void enc_prog(xmgn_workspace* ws, int blk, const float* io, long long row
     run_prog(ws, blk ? "enc_edge_fwd" : "enc_node_fwd", pr, (int)rows, nullptr, nullptr, false, st);
     return;
   }
-  s.epi = EPI_LN_BWD; s.flags = EF_COLSUM_ALL;
+  s.epi = EPI_LN_BWD; s.flags = blk == 0 ? EF_COLSUM_ALL : 0;   // edge rows: dgamma only (tile partials stay small)
   if (blk == 0) { s.f_in = ws->Gh; s.ld_in = H; s.valid_in = (int)rows; }
   else {
     s.flags |= EF_G16 | EF_NO_GA; s.g16 = ws->Ge[ws->gc_last].p; s.g16_lo = 0; s.valid_in = (int)rows;
@@ -902,7 +946,7 @@ static void enc_prog(xmgn_workspace* ws, int blk, const float* io, long long row
   for (int j = m; j >= 1; --j) {
     Step& d = pr.add();
     d.a_src = A_ACT; d.K = H; d.b_map = wH; d.b_row0 = (int)(io_D(m, blk, j) * H);
-    d.epi = EPI_DSILU; d.flags = EF_COLSUM_ALL | EF_DISCARD; d.vec0 = 3 + (m - j);
+    d.epi = EPI_DSILU; d.flags = (blk == 0 ? EF_COLSUM_ALL : 0) | EF_DISCARD; d.vec0 = 3 + (m - j);
     d.scr_s = ws->scrS[j - 1].p; d.scr_z = ws->scrZ[j - 1].p; d.lo_off = 0;
     d.in_map = pr.in_map(ws->scrS[j - 1].p, rows, H);
     if (j > 1) d.st_map = pr.in_map(ws->scrZ[j - 1].p, rows, H);
@@ -1044,9 +1088,15 @@ extern "C" xmgn_status xmgn_model_bwd(xmgn_workspace* ws, int part, const float*
       for (int v = 0; v < NV_MAX; ++v) d.off[v] = -1;
       d.off[0] = Io.gamma(blk); d.off[1] = Io.beta(blk); d.off[2] = Io.b(blk, m); d.off[3] = Io.b(blk, m - 1);
       if (m >= 2) d.off[4] = Io.b(blk, m - 2);
-      launch_reduce_colsum(ws->colsum, chain_grid(ws, (int)rows), NV_MAX, H, d, grad_io, st, ws->d_scale + 1);
-      for (int j = 1; j <= m; ++j)
-        wgrad(ws, ws->scrA[j - 1], none, H, H / 128, ws->scrZ[j], H, 0, rows, H, grad_io, Io.W(blk, j), st);
+      if (blk == 1) for (int v = 1; v < NV_MAX; ++v) d.off[v] = -1;   // edge rows: dgamma only
+      reduce_colsums(ws, d, grad_io, st);
+      for (int j = 1; j <= m; ++j)   // (edge rows: the biases ride on the weight-gradient GEMMs)
+        wgrad(ws, ws->scrA[j - 1], none, H, H / 128, ws->scrZ[j], H, 0, rows, H, grad_io, Io.W(blk, j), st,
+              blk == 1 ? Io.b(blk, j) : -1);
+      if (blk == 1) {
+        wgrad(ws, none, none, H, 0, ws->scrZ[0], H, 0, rows, 0, grad_io, 0, st, Io.b(blk, 0));        // db_0
+        wgrad(ws, none, none, H, 0, ws->Ge[ws->gc_last], H, 0, rows, 0, grad_io, 0, st, Io.beta(blk));  // dbeta
+      }
       const BfBuf& X = blk ? ws->Xe : ws->Xn;
       const long long nf = (long long)Io.fin(blk) * H;
       launch_wgrad_thin(ws->f16, Io.fin(blk), X.p, ws->scrZ[0].p, rows, H, ws->thin_part, st);
