@@ -142,7 +142,7 @@ constexpr int NV_MAX = 5;  // column-sum vectors per kernel
 // use four column groups (16 epilogue warps, latency tolerance); the FP32 check
 // mode keeps two (its hi/lo operands need the registers).
 #ifndef XMGN_CTRL_REGS
-#define XMGN_CTRL_REGS 56
+#define XMGN_CTRL_REGS 32   // control warps need < 32; the epilogue gets 112 (no spills), profiles/r02e_ab_ctrl_regs.jsonl
 #endif
 #ifndef XMGN_EPI_GROUPS
 #define XMGN_EPI_GROUPS 4
