@@ -1095,6 +1095,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
               mbar_wait(&acc_full2[hh], g & 1);
               tc_fence_after();
               mbar_wait(&act_rd[hh], g & 1);   // this step's MMAs no longer read ACT half hh
+              if (st_pending) {   // the previous step's TMA stores out of ACT half hh have read it
+                if (issuer) bulk_wait_read0();
+                named_bar(14 + hh, 256);
+                st_pending = false;
+              }
             } else {
             const int et = threadIdx.x - 128;
             for (int i = et; i < 3 * H; i += NEPI) {
@@ -1217,11 +1222,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
             }
             st_pending = true;
           }
-          // the next step refills the A ring (aliases ACT): drain before arriving
-          // (PIPE: always -- ACT half hh is handed back at the end of every step)
+          // the next step refills the A ring (aliases ACT): drain before arriving.  PIPE: only
+          // when the next step loads its A into ACT by TMA; otherwise the next step's MMA may read
+          // ACT while the stores still read it, and its epilogue drains them before rewriting ACT
           {
             const Step& nx = p.steps[s + 1 < p.n_steps ? s + 1 : 0];
-            if (st_pending && (PIPE || (nx.a_src == A_TMA && (nx.ctl & CTL_NEED_ACT_FREE)))) {
+            if (st_pending && (PIPE ? nx.a_src == A_TMA : (nx.a_src == A_TMA && (nx.ctl & CTL_NEED_ACT_FREE)))) {
               if (issuer) bulk_wait_read0();
               st_pending = false;
             }
@@ -1236,6 +1242,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
         else named_bar(8, NEPI + 32);
       }
     }
+    if (issuer) bulk_wait0();   // no TMA store may outlive the CTA's shared memory
   }
   tc_fence_before();
   __syncthreads();
