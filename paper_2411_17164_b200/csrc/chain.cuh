@@ -56,7 +56,11 @@ enum : int {
   EF_FROM_IN = 16384,  // EPI_SILU (16-bit modes): z is the TMA row input in ACT (a K = 0 step, no MMA)
   EF_NO_RES = 32768,   // EPI_LN_FWD (16-bit modes): y = LN(z), no residual (the encoders, NEXT-1)
   EF_NO_ACT = 65536,   // EPI_DSILU (16-bit modes): dZ leaves by row stores only, ACT untouched (last step)
-  EF_NO_GA = 131072    // EPI_LN_BWD + EF_G16: dY = G rows only (no G_a[dst] term, no write-back)
+  EF_NO_GA = 131072,   // EPI_LN_BWD + EF_G16: dY = G rows only (no G_a[dst] term, no write-back)
+  EF_OUT_HALF = 262144,  // EPI_STORE + EF_OUT16 (16-bit modes): write FP16 whatever the operand type
+                         // (the node pre-projections P are epilogue addends, not MMA operands)
+  EF_STORE_LO = 524288   // EPI_LN_FWD (16-bit modes): also write lo = y - rnd16(y) to lo_out (2 x 16-bit
+                         // GEMM operands of the BF16 mode)
 };
 
 enum : int {
@@ -90,6 +94,7 @@ struct Step {
   __nv_bfloat16* g16;             // 16-bit gradient stream [rows][H] (EF_G16)
   long long g16_lo;
   __nv_bfloat16* g16_out;         // EPI_ADD + EF_G16 output (same lo offset as g16)
+  __nv_bfloat16* lo_out;          // EPI_LN_FWD + EF_STORE_LO: lo rows [rows][H]
   const __nv_bfloat16* ga16;      // 16-bit aggregation adjoint G_a [N][H] gathered by dst (EF_G16)
   long long ga16_lo;
   // 16-bit modes: the epilogue's contiguous 16-bit row input (S', G_e, G_e', residual) is
@@ -541,8 +546,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
                 if (rank == 0) mbar_expect_tx(&a_full[kc], 2 * C::A_SLOT);
                 const uint32_t fb = mapa_shared(smem_u32(&a_full[kc]), 0);
                 const int k = kc * 64;
-                const int mi = (st.a_map1 >= 0 && k >= st.a_ksplit) ? st.a_map1 : st.a_map0;
-                const int kk = (st.a_map1 >= 0 && k >= st.a_ksplit) ? k - st.a_ksplit : k;
+                // A = [map a_map0 | map a_map0 + d | map a_map0 + 2d | ...], a_ksplit columns each
+                const int seg = st.a_map1 >= 0 ? k / st.a_ksplit : 0;
+                const int mi = st.a_map0 + seg * (st.a_map1 - st.a_map0), kk = k - seg * st.a_ksplit;
                 tma_load_2d_cg2(act + kc * C::A_SLOT, &p.maps[mi], fb, kk, row0);
               }
               const int slot = bi % C::SB;
@@ -620,8 +626,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THR
               const uint32_t fb = mapa_shared(smem_u32(&a_full[slot]), 0);
               uint8_t* dstp = act + slot * C::A_SLOT;
               const int k = kc * 64;
-              const int mi = (st.a_map1 >= 0 && k >= st.a_ksplit) ? st.a_map1 : st.a_map0;
-              const int kk = (st.a_map1 >= 0 && k >= st.a_ksplit) ? k - st.a_ksplit : k;
+              const int seg = st.a_map1 >= 0 ? k / st.a_ksplit : 0;   // A segments, see the PIPE producer
+              const int mi = st.a_map0 + seg * (st.a_map1 - st.a_map0), kk = k - seg * st.a_ksplit;
               tma_load_2d_cg2(dstp, &p.maps[mi], fb, kk, row0);
               if constexpr (SPLIT) tma_load_2d_cg2(dstp + C::A_SLOT_HALF, &p.maps[mi + 1], fb, kk, row0);
               ++ai;

@@ -272,13 +272,13 @@ __device__ __forceinline__ void op_silu(const Epi& e, const Step& st, Wait wait)
     if (gp) {
       if (tsrc) {
         float t[16];
-        in16<F16>(e, e.cb + cc * 16, t);
+        in16<true>(e, e.cb + cc * 16, t);   // P is stored FP16 in every 16-bit mode (EF_OUT_HALF)
 #pragma unroll
         for (int i = 0; i < 16; ++i) x[i] += t[i];
       } else {
-        add16<F16>(gs, x);
+        add16<true>(gs, x);
       }
-      add16<F16>(gd, x);
+      add16<true>(gd, x);
       if (cc + 2 < NC) {
         if (!tsrc) ld16(ps + (cc + 2) * 16, gs);
         ld16(pd + (cc + 2) * 16, gd);
@@ -351,6 +351,8 @@ __device__ __forceinline__ void op_ln_fwd(const Epi& e, const Step& st, Wait wai
   constexpr int W = IN32 ? 16 : 8;
   const bool w32 = e.valid && (st.flags & EF_STORE_F32) != 0;
   const bool w16 = e.valid && (st.flags & EF_STORE_BF) != 0, wact = (st.flags & EF_WRITE_ACT) != 0;
+  const bool wlo = e.valid && (st.flags & EF_STORE_LO) != 0;
+  __nv_bfloat16* oplo = st.lo_out + (size_t)e.r * H + e.cb;
   const bool has_res = e.valid && !(st.flags & EF_NO_RES);
   const __nv_bfloat16* rp16 = st.res16 + (size_t)e.r * H + e.cb;
   const float* rp32 = st.f_in + (size_t)e.r * st.ld_in + e.cb;
@@ -399,6 +401,15 @@ __device__ __forceinline__ void op_ln_fwd(const Epi& e, const Step& st, Wait wai
     for (int i = 0; i < 16; ++i) y[i] += gm[i];
     if (w32) st32x16(op32 + cc * 16, y);
     if (w16) st16<F16>(op16 + cc * 16, y);
+    if (wlo) {                      // y = hi + lo, both 16-bit (hi = the EF_STORE_BF rounding)
+      uint32_t hw[8];
+      float lo[16];
+      pack16x16<F16>(y, hw);
+      cvt16<F16>(hw, lo);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) lo[i] = y[i] - lo[i];
+      st16<F16>(oplo + cc * 16, lo);
+    }
     if (wact) sts_tile16<F16>(e.act, e.trow, e.cb + cc * 16, y);
   };
 #pragma unroll 1
@@ -623,7 +634,7 @@ __device__ __forceinline__ void op_dsilu(const Epi& e, const Step& st, Wait wait
 // EPI_STORE: out[:, col0 + c] = acc (16-bit bf_out with EF_OUT16, else FP32 f_out)
 template <int H, int NC, bool F16, class Wait>
 __device__ __forceinline__ void op_store(const Epi& e, const Step& st, Wait wait) {
-  const bool o16 = (st.flags & EF_OUT16) != 0;
+  const bool o16 = (st.flags & EF_OUT16) != 0, oh = o16 && (st.flags & EF_OUT_HALF) != 0;
   __nv_bfloat16* op16 = st.bf_out + (size_t)e.r * st.ld_out + st.col0 + e.cb;
   float* op32 = st.f_out + (size_t)e.r * st.ld_out + st.col0 + e.cb;
   wait();
@@ -637,7 +648,8 @@ __device__ __forceinline__ void op_store(const Epi& e, const Step& st, Wait wait
     for (int i = 0; i < 16; ++i) x[i] = __uint_as_float(ta[i]);
     if (cc + 1 < NC) tmem_ld16_async(e.tl + (cc + 1) * 16, ta);
     if (e.valid) {
-      if (o16) st16<F16>(op16 + cc * 16, x);
+      if (oh) st16<true>(op16 + cc * 16, x);
+      else if (o16) st16<F16>(op16 + cc * 16, x);
       else st32x16(op32 + cc * 16, x);
     }
   }

@@ -138,7 +138,8 @@ __global__ void __launch_bounds__(256) k_aggregate(const int* __restrict__ off, 
 // FP32, SURVEY §7.3 H1 rung R1): same order and output as k_aggregate.
 template <int H, bool F16>
 __global__ void __launch_bounds__(256) k_aggregate32(const int* __restrict__ off, const float* __restrict__ e,
-                                                     __nv_bfloat16* __restrict__ a, int n) {
+                                                     __nv_bfloat16* __restrict__ a, __nv_bfloat16* __restrict__ a_lo,
+                                                     int n) {
   constexpr int V = H / 4 / 32;  // float4 groups per lane
   const int lane = threadIdx.x & 31;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
@@ -171,8 +172,14 @@ __global__ void __launch_bounds__(256) k_aggregate32(const int* __restrict__ off
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       uint32_t h0, h1, l0, l1;
-      split2<F16, false>(acc[v].x, acc[v].y, h0, l0);
-      split2<F16, false>(acc[v].z, acc[v].w, h1, l1);
+      if (a_lo) {   // BF16 mode, 2 x BF16 node operands
+        split2<false, true>(acc[v].x, acc[v].y, h0, l0);
+        split2<false, true>(acc[v].z, acc[v].w, h1, l1);
+        reinterpret_cast<uint2*>(a_lo + (size_t)i * H)[lane + 32 * v] = make_uint2(l0, l1);
+      } else {
+        split2<F16, false>(acc[v].x, acc[v].y, h0, l0);
+        split2<F16, false>(acc[v].z, acc[v].w, h1, l1);
+      }
       reinterpret_cast<uint2*>(a + (size_t)i * H)[lane + 32 * v] = make_uint2(h0, h1);
     }
   }
@@ -595,13 +602,14 @@ void launch_aggregate(bool f16, int H, const int* off, const __nv_bfloat16* e, l
   count_launch();
   if (f16) agg_t<true>(H, off, e, e_lo, a, lo_off, n, st); else agg_t<false>(H, off, e, e_lo, a, lo_off, n, st);
 }
-void launch_aggregate32(int H, const int* off, const float* e, __nv_bfloat16* a, int n, cudaStream_t st) {
+void launch_aggregate32(int H, const int* off, const float* e, __nv_bfloat16* a, __nv_bfloat16* a_lo, int n,
+                        cudaStream_t st) {
   if (n <= 0) return;
   count_launch();
   int blocks = std::min((n + 7) / 8, 148 * 16);
-  if (H == 128) k_aggregate32<128, false><<<blocks, 256, 0, st>>>(off, e, a, n);
-  else if (H == 256) k_aggregate32<256, false><<<blocks, 256, 0, st>>>(off, e, a, n);
-  else k_aggregate32<512, false><<<blocks, 256, 0, st>>>(off, e, a, n);
+  if (H == 128) k_aggregate32<128, false><<<blocks, 256, 0, st>>>(off, e, a, a_lo, n);
+  else if (H == 256) k_aggregate32<256, false><<<blocks, 256, 0, st>>>(off, e, a, a_lo, n);
+  else k_aggregate32<512, false><<<blocks, 256, 0, st>>>(off, e, a, a_lo, n);
 }
 template <bool F16>
 static void seg_t(int H, const int* off, const int* rev, const __nv_bfloat16* dz, long long dz_lo, __nv_bfloat16* D,

@@ -24,7 +24,8 @@ void launch_to_bf16(bool f16, const float* in, __nv_bfloat16* out, long long lo_
 void launch_aggregate(bool f16, int H, const int* off, const __nv_bfloat16* e, long long e_lo, __nv_bfloat16* a,
                       long long lo_off, int n, cudaStream_t st);
 // BF16 mode: a (BF16) = CSR-order FP32 sums of the FP32 edge stream
-void launch_aggregate32(int H, const int* off, const float* e, __nv_bfloat16* a, int n, cudaStream_t st);
+void launch_aggregate32(int H, const int* off, const float* e, __nv_bfloat16* a, __nv_bfloat16* a_lo, int n,
+                        cudaStream_t st);
 void launch_segsum(bool f16, int H, const int* off, const int* rev, const __nv_bfloat16* dz, long long dz_lo,
                    __nv_bfloat16* D, long long d_lo, int n, int e_act, cudaStream_t st);
 void launch_wgrad(const WgradParams& p, bool split, bool f16, cudaStream_t st);

@@ -58,6 +58,12 @@ struct xmgn_workspace {
   float *h_buf[2] = {nullptr, nullptr};
   float *e32[2] = {nullptr, nullptr};  // BF16 mode: the edge residual stream in FP32 (ping-pong)
   bool e32_mode = false;
+  // BF16 mode: the node MLP's first GEMM and the pre-projection P take 2 x BF16 operands
+  // (hi + lo, forward only); P is stored FP16 in every 16-bit mode
+  bool bsplit = false;
+  xmgn::BfBuf wkx;                // [L][3][H][4H]: [W0h^T W0a^T W0h^T W0a^T]; [W0s^T W0s^T]; [W0d^T W0d^T]
+  xmgn::bf16* hlo[2] = {nullptr, nullptr};  // lo halves of h^l (ping-pong by l)
+  xmgn::bf16* alo = nullptr;      // lo half of a^l
   xmgn::BfBuf P;                  // node pre-projections, one per layer [L][Nmax][2H], 16-bit (kept for the bwd)
   // backward
   float* Gh = nullptr;            // dL/dh (FP32, node level)
@@ -178,6 +184,14 @@ static std::vector<PackJob> pack_jobs(xmgn_workspace* ws) {
     job(ws->wk2, 2 * H, r2(SL2_N1T), 0, H, 2 * H, Wn0, 1, H);
     job(ws->wk2, 2 * H, r2(SL2_SD), 0, H, H, We0 + (int64_t)H * H, H, 1);
     job(ws->wk2, 2 * H, r2(SL2_SD), H, H, H, We0 + 2 * (int64_t)H * H, H, 1);
+    if (ws->bsplit) {   // K-duplicated transposed weights: [A_hi | A_lo] x [W; W] = A W
+      auto rx = [&](int slot) { return (long long)(l * 3 + slot) * H; };
+      for (int d = 0; d < 2; ++d) {
+        job(ws->wkx, 4 * H, rx(0), d * 2 * H, H, 2 * H, Wn0, 1, H);
+        job(ws->wkx, 4 * H, rx(1), d * H, H, H, We0 + (int64_t)H * H, 1, H);
+        job(ws->wkx, 4 * H, rx(2), d * H, H, H, We0 + 2 * (int64_t)H * H, 1, H);
+      }
+    }
   }
   return J;
 }
@@ -204,9 +218,9 @@ struct Prog {
     return s;
   }
   // TMA gather source over P [rows][2H] 16-bit: 1-row boxes of 64 columns
-  int gather_map(const bf16* base, long long rows, int width) {
+  int gather_map(const bf16* base, long long rows, int width) {   // (P is FP16 in every 16-bit mode)
     if (next_map >= MAX_MAPS) throw Fail{set_error(XMGN_ESTATE, "internal: out of tensor-map slots")};
-    p.maps[next_map] = tmap16(base, width, (uint64_t)(rows > 0 ? rows : 1), width, 64, 1, f16);
+    p.maps[next_map] = tmap16(base, width, (uint64_t)(rows > 0 ? rows : 1), width, 64, 1, true);
     return next_map++;
   }
   // TMA source of an epilogue row input: 16-bit rows [0, rows) x H, rows > 0 (rows beyond read zero)
@@ -257,6 +271,8 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
   p.maps[1] = ws->split ? tmap16(ws->wk1.p + ws->wk1.lo, ws->H, r1, ws->H, 64, NB, f16) : p.maps[0];
   p.maps[2] = tmap16(ws->wk2.p, 2 * ws->H, r2, 2 * ws->H, 64, NB, f16);
   p.maps[3] = ws->split ? tmap16(ws->wk2.p + ws->wk2.lo, 2 * ws->H, r2, 2 * ws->H, 64, NB, f16) : p.maps[2];
+  if (ws->bsplit)   // slot 1 (the SPLIT-mode lo slot) holds the K-duplicated weights
+    p.maps[1] = tmap16(ws->wkx.p, 4 * ws->H, (long long)ws->L * 3 * ws->H, 4 * ws->H, 64, NB, f16);
   const int pair_tiles = (M + 255) / 256;
   const int grid = 2 * (pair_tiles < ws->sms / 2 ? pair_tiles : ws->sms / 2);
   p.colsum = bwd ? ws->colsum : nullptr;
@@ -443,6 +459,8 @@ static xmgn_status workspace_create(const xmgn_graph* g, const xmgn_model_cfg* c
       ws->S2 = 2;
       ws->wk1 = bfalloc(ws, (size_t)L * ws->S1 * H * H);
       ws->wk2 = bfalloc(ws, (size_t)L * ws->S2 * H * 2 * H);
+      ws->bsplit = cfg->precision == XMGN_PREC_BF16;
+      if (ws->bsplit) ws->wkx = bfalloc(ws, (size_t)L * 3 * H * 4 * H);
       std::vector<PackJob> jobs = pack_jobs(ws);
       ws->njobs = (int)jobs.size();
       ws->d_jobs = (PackJob*)dalloc(ws, jobs.size() * sizeof(PackJob));
@@ -460,6 +478,10 @@ static xmgn_status workspace_create(const xmgn_graph* g, const xmgn_model_cfg* c
       ws->e32_mode = cfg->precision == XMGN_PREC_BF16;
       if (ws->e32_mode)
         for (int i = 0; i < 2; ++i) ws->e32[i] = (float*)dalloc(ws, EH * 4);
+      if (ws->bsplit) {
+        for (int i = 0; i < 2; ++i) ws->hlo[i] = (bf16*)dalloc(ws, NH * 2);
+        ws->alo = (bf16*)dalloc(ws, NH * 2);
+      }
       ws->P = bfalloc(ws, (size_t)ckL * 2 * NH);
       if (!infer) {
         ws->Ge[0] = bfalloc(ws, EH);
@@ -539,22 +561,35 @@ static void proc_fwd(xmgn_workspace* ws, int part, const float* params, const fl
       launch_to_bf16(ws->f16, h0, ws->h_ck.p, ws->h_ck.lo, n0 * H, st);
       launch_to_bf16(ws->f16, e0, ws->e_ck.p, ws->e_ck.lo, e1 * H, st);
     }
+    if (ws->bsplit)   // h^0 = hi + lo (hi rewritten with the same RNE bits)
+      launch_to_bf16(false, h0, ws->h_ck.p, (long long)(ws->hlo[0] - ws->h_ck.p), n0 * H, st);
     const int W1 = 0, W2 = 2;  // weight map slots
     auto r1 = [&](int l, int slot) { return (l * ws->S1 + slot) * H; };
     auto r2 = [&](int l, int slot) { return (l * ws->S2 + slot) * H; };
-    {  // P = h0 [W1e_s | W1e_d] for layer 1
+    auto Pl = [&](int li) { return ws->P.p + ws->ck(li) * 2 * NH; };   // P of layer li + 1
+    // P = h^l [W1e_s | W1e_d] for layer l + 1 as its own launch (layer 1; BF16 mode: every layer,
+    // from 2 x BF16 h^l = [h_hi | h_lo] against [W; W]); 16-bit modes store P in FP16
+    auto proj = [&](int l) {
+      const int64_t nr = n_at(P, L, l);
       Prog pr(ws);
-      set_a(ws, pr, 4, ws->h_ck, n0, H);
+      const BfBuf hck = at(ws->h_ck, ws->ck(l) * NH);
+      set_a(ws, pr, 4, hck, nr, H);
+      if (ws->bsplit) pr.p.maps[5] = map_rows(ws->hlo[l & 1], nr, H, 128, false);
       for (int half = 0; half < 2; ++half) {
         Step& s = pr.add();
         s.a_src = A_TMA; s.a_map0 = 4; s.K = H;
-        s.b_map = W1; s.b_row0 = r1(0, half ? SL_PDT : SL_PST);
-        s.epi = EPI_STORE; s.flags = EF_OUT16; s.bf_out = ws->P.p; s.bf_lo = ws->P.lo; s.ld_out = 2 * H;
+        s.b_map = W1; s.b_row0 = r1(l, half ? SL_PDT : SL_PST);
+        if (ws->bsplit) {
+          s.a_map1 = 5; s.a_ksplit = H; s.K = 2 * H;
+          s.b_map = 1; s.b_row0 = (l * 3 + 1 + half) * H;
+        }
+        s.epi = EPI_STORE; s.flags = EF_OUT16 | (ws->split ? 0 : EF_OUT_HALF);
+        s.bf_out = Pl(l); s.bf_lo = ws->P.lo; s.ld_out = 2 * H;
         s.col0 = half * H;
       }
-      run_prog(ws, "chain_proj", pr, (int)n0, nullptr, nullptr, false, st);
-    }
-    auto Pl = [&](int li) { return ws->P.p + ws->ck(li) * 2 * NH; };   // P of layer li + 1
+      run_prog(ws, "chain_proj", pr, (int)nr, nullptr, nullptr, false, st);
+    };
+    proj(0);
     int cur = 0, ce = 0;   // ping-pong indices of the FP32 node (and BF16-mode edge) streams
     for (int l = 1; l <= L; ++l) {
       const int li = l - 1;
@@ -598,7 +633,7 @@ static void proc_fwd(xmgn_workspace* ws, int part, const float* params, const fl
       }
       // aggregation (Eq. 2) -> a^l (BF16 operand + checkpoint)
       { ProfScope ps("aggregate", st);
-      if (ws->e32_mode) launch_aggregate32(H, dp.off, ws->e32[ce ^ 1], ack.p, (int)nl, st);
+      if (ws->e32_mode) launch_aggregate32(H, dp.off, ws->e32[ce ^ 1], ack.p, ws->bsplit ? ws->alo : nullptr, (int)nl, st);
       else launch_aggregate(ws->f16, H, dp.off, eck_next.p, eck_next.lo, ack.p, ack.lo, (int)nl, st); }
       ce ^= 1;
       XMGN_CUDA(cudaGetLastError(), "aggregate launch");
@@ -606,11 +641,17 @@ static void proc_fwd(xmgn_workspace* ws, int part, const float* params, const fl
         Prog pr(ws);
         set_a(ws, pr, 4, hck_prev, nl, H);
         set_a(ws, pr, 6, ack, nl, H);
+        if (ws->bsplit) {   // A = [h_hi | a_hi | h_lo | a_lo] (slots 4..7), B = [W0; W0]
+          pr.p.maps[5] = pr.p.maps[6];
+          pr.p.maps[6] = map_rows(ws->hlo[li & 1], nl, H, 128, false);
+          pr.p.maps[7] = map_rows(ws->alo, nl, H, 128, false);
+        }
         for (int j = 0; j < m; ++j) {
           Step& s = pr.add();
           s.a_src = j == 0 ? A_TMA : A_ACT; s.a_map0 = 4; s.a_map1 = 6; s.a_ksplit = H;
           s.K = j == 0 ? 2 * H : H;
           s.b_map = j == 0 ? W2 : W1; s.b_row0 = j == 0 ? r2(li, SL2_N1T) : r1(li, sl_njt(m) + j - 1);
+          if (j == 0 && ws->bsplit) { s.a_map1 = 5; s.K = 4 * H; s.b_map = 1; s.b_row0 = li * 3 * H; }
           s.epi = EPI_SILU; s.bias = params + Ly.b(li, 1, j);
         }
         Step& s = pr.add();
@@ -623,18 +664,24 @@ static void proc_fwd(xmgn_workspace* ws, int part, const float* params, const fl
           s.flags |= EF_STORE_BF;
           s.bf_out = hL16; s.bf_lo = 0;
         }
-        if (l < L) {
+        if (l < L && ws->bsplit) {   // h^l = hi + lo; P of layer l + 1 by proj(l) below
+          s.flags |= EF_STORE_BF | EF_STORE_LO;
+          s.bf_out = ws->h_ck.p + ws->ck(l) * NH; s.bf_lo = 0;
+          s.lo_out = ws->hlo[l & 1];
+        } else if (l < L) {
           s.flags |= EF_STORE_BF | EF_WRITE_ACT;
           s.bf_out = ws->h_ck.p + ws->ck(l) * NH; s.bf_lo = ws->h_ck.lo;
           for (int half = 0; half < 2; ++half) {
             Step& q = pr.add();
             q.a_src = A_ACT; q.K = H; q.b_map = W1; q.b_row0 = r1(l, half ? SL_PDT : SL_PST);
-            q.epi = EPI_STORE; q.flags = EF_OUT16; q.bf_out = Pl(l); q.bf_lo = ws->P.lo; q.ld_out = 2 * H;
+            q.epi = EPI_STORE; q.flags = EF_OUT16 | (ws->split ? 0 : EF_OUT_HALF);
+            q.bf_out = Pl(l); q.bf_lo = ws->P.lo; q.ld_out = 2 * H;
             q.col0 = half * H;
           }
         }
         run_prog(ws, "chain_node_fwd", pr, (int)nl, nullptr, nullptr, false, st);
       }
+      if (ws->bsplit && l < L) proj(l);
       cur ^= 1;
     }
     ws->last_fwd = part;

@@ -153,12 +153,12 @@ def test_check_finite_and_state_errors():
     pr.close()
 
 
-# BF16 operands (8-bit mantissa) at 15 layers on CFG2's 12.8M outputs: max|dh| / RMS measured
-# 2.02e-2 (round 1, 16-bit edge stream) and 2.23e-2 (FP32 edge stream) -- just above north_star's
-# 2e-2, as SURVEY §7.3 H1's emulation predicted (1.9-2.1e-2, growing with N).  The production mode
-# is FP16 (same MMA rate, 3 more mantissa bits, 3.6e-3 here); BF16 is held to the measured level
-# so a regression still fails.
-TAU_CFG2_L15 = {FP16: 2e-2, BF16: 3e-2}
+# BF16 operands (8-bit mantissa) at 15 layers on CFG2's 12.8M outputs: with every operand a
+# single BF16 the max|dh| / RMS was 2.23e-2, just above north_star's 2e-2 (SURVEY §7.3 H1's
+# emulation: 1.9-2.1e-2, growing with N).  The BF16 mode now stores P in FP16 and feeds the
+# node MLP's first GEMM and the pre-projection 2 x BF16 operands (hi + lo against [W; W]);
+# scratch/bf16_emul.py predicts 1.6e-2 at N = 100k.  Both modes are held to north_star's bound.
+TAU_CFG2_L15 = {FP16: 2e-2, BF16: 2e-2}
 
 
 @pytest.mark.slow
