@@ -22,7 +22,12 @@ static void chain_launch(const ChainParams& p, int grid, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
     if (dev >= 0 && dev < 64) attr[dev].store(true, std::memory_order_release);
   }
-  kern<<<grid, EpiShape<SPLIT>::THREADS, C::SMEM_BYTES, st>>>(p);
+  kern<<<grid, EpiShape<H, SPLIT>::THREADS, C::SMEM_BYTES, st>>>(p);
+}
+
+int chain_ctas_per_sm(int H, bool split) {
+  if (H == 128) return split ? EpiShape<128, true>::MINB : EpiShape<128, false>::MINB;
+  return H == 256 ? EpiShape<256, false>::MINB : EpiShape<512, false>::MINB;
 }
 
 size_t chain_smem(int H, bool split) {

@@ -152,14 +152,25 @@ constexpr int NV_MAX = 5;  // column-sum vectors per kernel
 #ifndef XMGN_EPI_GROUPS
 #define XMGN_EPI_GROUPS 4
 #endif
-template <bool SPLIT>
+// H = 128 (16-bit modes): four CTAs per SM (four pair-tiles in flight per SM pair, so one tile's
+// TMA / MMA / epilogue latency chain overlaps the others'), one column group each (all four
+// fit: 4 x 128 TMEM columns, 4 x 56 KB smem with a 2-slot B ring).  CFG2 step (1 B200, FP16):
+// 1 CTA/SM 42.3 ms, 2 (two groups) 33.6 ms, 3 31.1 ms, 4 30.7 ms (profiles/r03e_ab_ctas128.txt).
+#ifndef XMGN_CTAS128
+#define XMGN_CTAS128 4
+#endif
+#ifndef XMGN_EW128
+#define XMGN_EW128 1
+#endif
+template <int H, bool SPLIT>
 struct EpiShape {
-  static constexpr int EW = SPLIT ? 2 : XMGN_EPI_GROUPS;
+  static constexpr int MINB = (H == 128 && !SPLIT) ? XMGN_CTAS128 : 1;   // CTAs per SM
+  static constexpr int EW = SPLIT ? 2 : (MINB > 1 ? XMGN_EW128 : XMGN_EPI_GROUPS);
   static constexpr int THREADS = 128 + 128 * EW;
   // setmaxnreg split.  The CTA owns exactly THREADS x LAUNCH_REGS registers (the
   // count ptxas derives from __launch_bounds__); setmaxnreg.inc can only take what
   // the control warpgroup released with setmaxnreg.dec, or it blocks forever.
-  static constexpr int LAUNCH_REGS = (65536 / THREADS) & ~7;
+  static constexpr int LAUNCH_REGS = (65536 / (THREADS * MINB)) & ~7;
   static constexpr int CTRL_REGS = XMGN_CTRL_REGS;   // control warps after setmaxnreg.dec
   static constexpr int EPI_REGS_FIT = (LAUNCH_REGS + (LAUNCH_REGS - CTRL_REGS) / EW) & ~7;
   static constexpr int EPI_REGS = EPI_REGS_FIT > 224 ? 224 : EPI_REGS_FIT;
@@ -193,13 +204,14 @@ struct ChainCfg {
   static constexpr int SA = ACT_BYTES / A_SLOT;
   static constexpr uint32_t B_SLOT_HALF = NBH * 128u;
   static constexpr uint32_t B_SLOT = F * B_SLOT_HALF;
-  static constexpr uint32_t SMEM_LIMIT = 227u * 1024u;
+  static constexpr uint32_t SMEM_LIMIT =
+      EpiShape<H, SPLIT>::MINB > 1 ? 228u * 1024u / EpiShape<H, SPLIT>::MINB - 1024u : 227u * 1024u;
   static constexpr uint32_t PRM_BYTES = 2u * 3u * H * 4u;        // per-step bias/gamma/beta, double-buffered
-  static constexpr int SB_FIT = (int)((SMEM_LIMIT - 1536u - 512u * EpiShape<SPLIT>::EW - PRM_BYTES - ACT_BYTES) / B_SLOT);
+  static constexpr int SB_FIT = (int)((SMEM_LIMIT - 1536u - 512u * EpiShape<H, SPLIT>::EW - PRM_BYTES - ACT_BYTES) / B_SLOT);
   static constexpr int SB = SB_FIT > 8 ? 8 : SB_FIT;
   static constexpr uint32_t BAR_OFF = ACT_BYTES + SB * B_SLOT;
   static constexpr uint32_t RED_OFF = BAR_OFF + 512;             // row-reduction exchange [EW][128] f32
-  static constexpr uint32_t PRM_OFF = RED_OFF + EpiShape<SPLIT>::EW * 128 * 4;
+  static constexpr uint32_t PRM_OFF = RED_OFF + EpiShape<H, SPLIT>::EW * 128 * 4;
   static constexpr uint32_t SMEM_BYTES = PRM_OFF + PRM_BYTES + 1024;  // + alignment slack
   static constexpr uint32_t TMEM_COLS = H;
   static_assert(SB >= 2, "B ring too small");
@@ -428,13 +440,13 @@ struct TileSched {   // everything but the queue base is re-derived at each call
 // An A_TMA step stages its A chunk kc straight into ACT block kc (all K = H resident, read by
 // both N-halves).  LayerNorm steps still need both halves' row statistics (row_sum).
 template <int H, bool SPLIT, bool BWD, bool F16, bool Z1 = false, bool PIPE = false, int OPS = OPS_ALL>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<SPLIT>::THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<H, SPLIT>::THREADS, EpiShape<H, SPLIT>::MINB)
     k_chain(const __grid_constant__ ChainParams p) {
-  static_assert(!PIPE || (H == 512 && !SPLIT && !Z1 && EpiShape<SPLIT>::EW == 4), "PIPE: H = 512, 16-bit, 4 groups");
+  static_assert(!PIPE || (H == 512 && !SPLIT && !Z1 && EpiShape<H, SPLIT>::EW == 4), "PIPE: H = 512, 16-bit, 4 groups");
   using C = ChainCfg<H, SPLIT>;
   constexpr int NB = C::NB;
   constexpr int NH = H / NB;           // N-halves per step
-  using ES = EpiShape<SPLIT>;
+  using ES = EpiShape<H, SPLIT>;
   constexpr int EW = ES::EW;
   constexpr int HC = H / EW;           // columns per epilogue warp
   constexpr int NC = HC / 32;          // 32-column chunks per epilogue warp

@@ -343,12 +343,29 @@ __global__ void __launch_bounds__(256, 4) k_segsum16(const int* __restrict__ off
 // copies exist.  gridDim = (Hin/128, Hout/NT, n_split); each CTA reduces a
 // fixed row range and writes its FP32 partial; k_reduce_part sums the splits
 // in order.
+// H = 128 (NT = 128, 16-bit): XMGN_WGRAD_CTAS128 CTAs per SM with a shallower ring.  Two per SM
+// made the CFG2 wgrads 5% slower (profiles/r03f_ab_wgrad128.txt), so the default stays at one.
+#ifndef XMGN_WGRAD_CTAS128
+#define XMGN_WGRAD_CTAS128 1
+#endif
+template <int NT, bool SPLIT>
+struct WgradShape {
+  static constexpr int F = SPLIT ? 2 : 1;
+  static constexpr int MINB = (NT == 128 && !SPLIT) ? XMGN_WGRAD_CTAS128 : 1;
+  static constexpr uint32_t STAGE = F * (128 * 64 * 2 + NT * 64 * 2);
+  static constexpr uint32_t BUDGET = 220u * 1024u / MINB;
+  static constexpr int S = (int)(BUDGET / STAGE) > 6 ? 6 : (int)(BUDGET / STAGE);
+  static constexpr size_t SMEM = 1024 + S * STAGE + 256;
+};
+int wgrad_ctas_per_sm(int H, bool split) { return H == 128 ? (split ? 1 : XMGN_WGRAD_CTAS128) : 1; }
+
 template <int NT, bool SPLIT, bool F16>
-__global__ void __launch_bounds__(128, 1) k_wgrad(const __grid_constant__ WgradParams p) {
+__global__ void __launch_bounds__(128, (WgradShape<NT, SPLIT>::MINB)) k_wgrad(const __grid_constant__ WgradParams p) {
   constexpr int F = SPLIT ? 2 : 1;
   constexpr uint32_t A_HALF = 128 * 64 * 2, B_HALF = NT * 64 * 2;
   constexpr uint32_t STAGE = F * (A_HALF + B_HALF);
-  constexpr int S = (int)((220u * 1024u) / STAGE) > 6 ? 6 : (int)((220u * 1024u) / STAGE);
+  static_assert(STAGE == WgradShape<NT, SPLIT>::STAGE, "stage size");
+  constexpr int S = WgradShape<NT, SPLIT>::S;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE);
@@ -635,10 +652,7 @@ void launch_segsum(bool f16, int H, const int* off, const int* rev, const __nv_b
 
 template <int NT, bool SPLIT, bool F16>
 static void wgrad_launch(const WgradParams& p, dim3 grid, cudaStream_t st) {
-  constexpr int F = SPLIT ? 2 : 1;
-  constexpr uint32_t STAGE = F * (128 * 64 * 2 + NT * 64 * 2);
-  constexpr int S = (int)((220u * 1024u) / STAGE) > 6 ? 6 : (int)((220u * 1024u) / STAGE);
-  size_t smem = 1024 + S * STAGE + 256;
+  const size_t smem = WgradShape<NT, SPLIT>::SMEM;
   auto kern = k_wgrad<NT, SPLIT, F16>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, 128, smem, st>>>(p);

@@ -234,6 +234,13 @@ struct Prog {
 
 static bool epi_writes_act(const Step& s) { return step_writes_act(s); }
 
+// persistent grid: one cluster (CTA pair) per SM pair and resident CTA slot, at most one per pair tile
+static int chain_grid(xmgn_workspace* ws, int M) {
+  const int pair_tiles = (M + 255) / 256;
+  const int slots = ws->sms / 2 * chain_ctas_per_sm(ws->H, ws->split);
+  return 2 * (pair_tiles < slots ? pair_tiles : slots);
+}
+
 // Derive the ACT hand-off controls (chain.cuh) and launch.
 static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, const int* src, const int* dst, bool bwd,
                      cudaStream_t st) {
@@ -273,8 +280,8 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
   p.maps[3] = ws->split ? tmap16(ws->wk2.p + ws->wk2.lo, 2 * ws->H, r2, 2 * ws->H, 64, NB, f16) : p.maps[2];
   if (ws->bsplit)   // slot 1 (the SPLIT-mode lo slot) holds the K-duplicated weights
     p.maps[1] = tmap16(ws->wkx.p, 4 * ws->H, (long long)ws->L * 3 * ws->H, 4 * ws->H, 64, NB, f16);
+  const int grid = chain_grid(ws, M);
   const int pair_tiles = (M + 255) / 256;
-  const int grid = 2 * (pair_tiles < ws->sms / 2 ? pair_tiles : ws->sms / 2);
   p.colsum = bwd ? ws->colsum : nullptr;
   if (bwd) {
     // column-sum vectors this program writes -> consecutive slots of per-tile partials (each
@@ -308,10 +315,7 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
   XMGN_CUDA(cudaGetLastError(), "chain kernel launch");
 }
 
-static int chain_grid(xmgn_workspace* ws, int M) {
-  const int pair_tiles = (M + 255) / 256;
-  return 2 * (pair_tiles < ws->sms / 2 ? pair_tiles : ws->sms / 2);
-}
+
 
 static void set_a(xmgn_workspace* ws, Prog& pr, int slot, const BfBuf& b, long long rows, int width) {
   pr.p.maps[slot] = map_rows(b.p, rows, width, 128, ws->f16);
@@ -349,8 +353,8 @@ static void wgrad(xmgn_workspace* ws, const BfBuf& a0, const BfBuf& a1, int a_wi
   const int NT = H >= 256 ? 256 : H;
   const int tiles = (Hin / 128 + (p.ones_tile ? 1 : 0)) * (H / NT);
   const int chunks = (int)((rows + 63) / 64);
-  // one wave: every CTA holds a 1-CTA/SM smem ring, so tiles x S <= SMs (no tail wave)
-  int S = ws->sms / tiles;
+  // one wave: tiles x S <= SMs x resident CTAs per SM (no tail wave)
+  int S = ws->sms * wgrad_ctas_per_sm(H, ws->split) / tiles;
   if (S > chunks) S = chunks;
   if (S > ws->part_splits) S = ws->part_splits;
   if (S < 1) S = 1;
@@ -491,7 +495,7 @@ static xmgn_status workspace_create(const xmgn_graph* g, const xmgn_model_cfg* c
         for (int j = 0; j < m; ++j) { ws->scrA[j] = bfalloc(ws, RH); ws->scrS[j] = bfalloc(ws, RH); }
         for (int j = 0; j <= m; ++j) ws->scrZ[j] = bfalloc(ws, RH);
         ws->D = bfalloc(ws, 2 * NH);
-        ws->part_splits = 64;
+        ws->part_splits = 64;   // more splits cost more in k_reduce_part than they save (r03f)
         ws->part = (float*)dalloc(ws, (size_t)ws->part_splits * (2 * H + 128) * H * 4);
         // per-tile partials: edge programs write one vector (dgamma), node programs up to NV_MAX
         const size_t nct_e = 2 * (size_t)((ws->Emax + 255) / 256), nct_n = 2 * (size_t)((ws->Nmax + 255) / 256);
