@@ -177,6 +177,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-model", action="store_true")
+    ap.add_argument("--no-bf16-leg", action="store_true")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "xmgn":
         return relaunch(args.gpus)
@@ -436,6 +437,35 @@ def main():
                  "h2d_bytes_per_step": mbi, "d2h_bytes_per_step": 4, "loss": float(loss_host.item()),
                  "processor_share": round(ms / mms, 4)}
 
+    # ---- the same processor step with BF16 operands (north_star's precision; the FP16 headline
+    # runs the same tcgen05 kind::f16 datapath): a fresh BF16 workspace, 1 warm-up + 2 timed steps
+    bf16_leg = None
+    if args.precision == "fp16" and not args.no_bf16_leg:
+        if e2e is None and model is None:
+            del inputs
+        pr.close()
+        torch.cuda.empty_cache()
+        pr = Processor(bundle, Hc, Lc, m=M_HID, precision=xmgn.PREC_BF16, device=local, parts=parts,
+                       halo_depth=Lc)
+        inputs = {p: pr.make_inputs(p) for p in parts}
+        step()
+        sync_all()
+        k5 = max(1, min(args.steps, 2))
+        ev0.record(stream)
+        for _ in range(k5):
+            step()
+        ev1.record(stream)
+        sync_all()
+        t5 = torch.tensor([ev0.elapsed_time(ev1) / k5], device=dev)
+        if world > 1:
+            dist.all_reduce(t5, op=dist.ReduceOp.MAX)
+        bms = float(t5.item())
+        bf16_leg = {"dtype": "bf16", "value": E_global / (bms / 1e3), "unit": "edges/s", "ms_per_step": bms,
+                    "steps": k5, "note": "BF16 operands (FP32 edge stream, FP16 P, 2 x BF16 node first-GEMM "
+                                         "and pre-projection operands): max|dh|/RMS 1.6e-2 <= 2e-2 at L = 15 "
+                                         "(DESIGN.md section 3)"}
+        del inputs
+
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -457,7 +487,8 @@ def main():
                        "edges_global": E_global, "partitions": P, "partitions_per_gpu": len(parts),
                        "parallelism": f"halo-partition dp{world}", "l2": "inputs larger than L2 (no flush)",
                        "graph_build_s": round(t_gen, 1)},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "model_step": model, "clocks": clocks,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "model_step": model, "bf16_step": bf16_leg,
+            "clocks": clocks,
             "gpu_launches": launches,
             "alg_tflops_per_s": round(float(t2.item()) * args.steps / (ms * args.steps / 1e3) / 1e12, 2),
             "scopes": scopes,

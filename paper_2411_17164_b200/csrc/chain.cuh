@@ -189,6 +189,13 @@ struct ChainParams {
   int cs_slot[NV_MAX];    // column-sum vector -> slot (-1: the program never writes it)
   float eps;          // LayerNorm epsilon
   int* tile_counter;  // dynamic tile scheduler: zeroed before the launch (null = static tiles)
+  // static parameter table (16-bit modes): when the program's distinct bias / gamma / beta
+  // vectors fit the PRM region (n_prm > 0), they are staged in shared memory ONCE per launch
+  // (prm_src[i] -> table row i, null = zeros) and step s reads rows prm_slot[s][0..2]; else
+  // (n_prm = 0) every step re-stages its three vectors before waiting for its accumulator
+  int n_prm;
+  const float* prm_src[6];
+  signed char prm_slot[MAX_STEPS][3];
 };
 constexpr int TQ = 2;   // tile-queue slots per cluster (the producer claims at most one tile ahead)
 
@@ -512,6 +519,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<H, SPLIT>::
   }
   if (w == 0 && lane_id() == 0)
     for (int i = 0; i < MAX_MAPS; ++i) tma_prefetch(&p.maps[i]);
+  if (!SPLIT && p.n_prm > 0)
+    for (int i = threadIdx.x; i < p.n_prm * H; i += blockDim.x) {
+      const float* v = p.prm_src[i / H];
+      prm_base[i] = v ? __ldg(v + (i % H)) : 0.f;
+    }
   if (w == 2) tmem_alloc_cg2(tslot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
@@ -1103,13 +1115,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<H, SPLIT>::
           auto wait = [&]() {
             if constexpr (PIPE) {
               // this N-half's 256 threads stage its 256 columns of bias / gamma / beta
-              const int et = threadIdx.x - 128 - 256 * hh;
-              for (int i = et; i < 3 * 256; i += 256) {
-                const int vec = i >> 8, c = 256 * hh + (i & 255);
-                const float* srcv = vec == 0 ? st.bias : (vec == 1 ? st.gamma : st.beta);
-                prm[vec * H + c] = srcv ? __ldg(srcv + c) : 0.f;
+              if (p.n_prm == 0) {
+                const int et = threadIdx.x - 128 - 256 * hh;
+                for (int i = et; i < 3 * 256; i += 256) {
+                  const int vec = i >> 8, c = 256 * hh + (i & 255);
+                  const float* srcv = vec == 0 ? st.bias : (vec == 1 ? st.gamma : st.beta);
+                  prm[vec * H + c] = srcv ? __ldg(srcv + c) : 0.f;
+                }
+                named_bar(5 + hh, 256);
               }
-              named_bar(5 + hh, 256);
               mbar_wait(&acc_full2[hh], g & 1);
               tc_fence_after();
               mbar_wait(&act_rd[hh], g & 1);   // this step's MMAs no longer read ACT half hh
@@ -1119,12 +1133,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<H, SPLIT>::
                 st_pending = false;
               }
             } else {
-            const int et = threadIdx.x - 128;
-            for (int i = et; i < 3 * H; i += NEPI) {
-              const float* srcv = i < H ? st.bias : (i < 2 * H ? st.gamma : st.beta);
-              prm[i] = srcv ? __ldg(srcv + (i % H)) : 0.f;
+            if (p.n_prm == 0) {
+              const int et = threadIdx.x - 128;
+              for (int i = et; i < 3 * H; i += NEPI) {
+                const float* srcv = i < H ? st.bias : (i < 2 * H ? st.gamma : st.beta);
+                prm[i] = srcv ? __ldg(srcv + (i % H)) : 0.f;
+              }
+              named_bar(7, NEPI);
             }
-            named_bar(7, NEPI);
             mbar_wait(acc_full, g & 1);
             tc_fence_after();
             if (st_pending) {   // the previous step's stores must have read ACT before anything rewrites it
@@ -1169,7 +1185,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<H, SPLIT>::
           };
           Epi e;
           e.act = act; e.tl = tl; e.trow = trow; e.cb = cb; e.r = r; e.src = src; e.dst = dst; e.valid = valid;
-          e.sb = prm + cb; e.sg = prm + H + cb; e.sbt = prm + 2 * H + cb; e.colsum = colsum_base; e.cs_vstride = (size_t)p.cs_vstride; e.cs_slot = p.cs_slot; e.eps = p.eps;
+          if (p.n_prm > 0) {
+            e.sb = prm_base + p.prm_slot[s][0] * H + cb;
+            e.sg = prm_base + p.prm_slot[s][1] * H + cb;
+            e.sbt = prm_base + p.prm_slot[s][2] * H + cb;
+          } else {
+            e.sb = prm + cb; e.sg = prm + H + cb; e.sbt = prm + 2 * H + cb;
+          } e.colsum = colsum_base; e.cs_vstride = (size_t)p.cs_vstride; e.cs_slot = p.cs_slot; e.eps = p.eps;
           e.in_full = in_full; e.in_par = nin & 1; e.pol_last = pol_last;
           constexpr int NC16 = HC / 16;
           const int op = st.epi;

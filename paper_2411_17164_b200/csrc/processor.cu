@@ -100,6 +100,7 @@ struct xmgn_workspace {
   int head_warps = 0;
   bool infer = false;   // inference workspace: forward only, per-layer buffers ping-ponged
   bool pipe = true;     // N-half-pipelined chain kernel where a program allows it (XMGN_PIPE=0: off)
+  bool prm_table = true;  // per-launch static bias/gamma/beta table in the chain kernels (XMGN_PRM_TABLE=0: off)
   bool dyn = false;     // dynamic tile scheduling in the chain kernels (XMGN_DYN=1, needs XMGN_STATIC_TILES=0)
   int* d_tile_counter = nullptr;
   // checkpoint slot of layer l's tensors (training: one per layer; inference: ping-pong)
@@ -270,6 +271,28 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
       if (used) S.ctl |= CTL_NEED_ACT_FREE;
     }
   }
+  // static parameter table (chain.cuh ChainParams::n_prm): the program's distinct bias / gamma /
+  // beta vectors (null = one zero row) if they fit the kernel's 6-row PRM region
+  {
+    p.n_prm = 0;
+    int n = 0;
+    bool fits = !ws->split && ws->prm_table;
+    for (int s = 0; s < pr.n && fits; ++s) {
+      const float* v3[3] = {p.steps[s].bias, p.steps[s].gamma, p.steps[s].beta};
+      for (int k = 0; k < 3 && fits; ++k) {
+        int slot = -1;
+        for (int i = 0; i < n; ++i)
+          if (p.prm_src[i] == v3[k]) slot = i;
+        if (slot < 0) {
+          if (n == 6) { fits = false; break; }
+          p.prm_src[n] = v3[k];
+          slot = n++;
+        }
+        p.prm_slot[s][k] = (signed char)slot;
+      }
+    }
+    if (fits) p.n_prm = n;
+  }
   // weight maps
   const int NB = (ws->H < 256 ? ws->H : 256) / 2;   // B rows per CTA of a pair
   const long long r1 = (long long)ws->L * ws->S1 * ws->H, r2 = (long long)ws->L * ws->S2 * ws->H;
@@ -433,6 +456,7 @@ static xmgn_status workspace_create(const xmgn_graph* g, const xmgn_model_cfg* c
       ws->cfg = *cfg;
       ws->infer = infer;
       { const char* pe = getenv("XMGN_PIPE"); ws->pipe = !(pe && atoi(pe) == 0); }
+      { const char* pt = getenv("XMGN_PRM_TABLE"); ws->prm_table = !(pt && atoi(pt) == 0); }
       { const char* de = getenv("XMGN_DYN"); ws->dyn = de && atoi(de) == 1; }   // see XMGN_STATIC_TILES
       ws->dev = g->device;
       ws->H = H; ws->L = L; ws->m = m;
