@@ -79,6 +79,16 @@ def cpu_cores():
     return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 # ---------------------------------------------------------------- clocks
 class Clocks:
     def __init__(self, device):
@@ -471,7 +481,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         lg = oracle_sample(bundle, 2500)
         ts = time_oracle(lg, Hc, Lc)
-        cpu = {"value": len(lg["sources"]) / ts[0], "unit": "edges/s", "cores": cpu_cores(), "kind": "oracle",
+        cpu = {"value": len(lg["sources"]) / ts[0], "unit": "edges/s", "cores": cpu_cores(), "cpu_model": cpu_model(), "kind": "oracle",
                "sample": f"FP64 oracle fwd+bwd, {Lc} layers, H={Hc}, on a {len(lg['sources'])}-edge "
                          f"{len(lg['gid'])}-node BFS ball of the {args.config} graph ({ts[0]:.1f} s)"}
 
@@ -520,7 +530,7 @@ def reference(args, world, rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": s * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config} (bounded sample)", "parallelism": "host cores"},
-            "cpu_baseline": {"value": v, "unit": "edges/s", "cores": cpu_cores(), "kind": "oracle",
+            "cpu_baseline": {"value": v, "unit": "edges/s", "cores": cpu_cores(), "cpu_model": cpu_model(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

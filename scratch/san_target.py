@@ -10,8 +10,10 @@ from paper_2411_17164_b200.processor import Processor
 
 b = configs.custom((300, 1200), k=6, P=2, halo=2)
 st = torch.cat([torch.zeros(28), torch.ones(28)]).cuda()
+import os
+PREC = xmgn.PREC_BF16 if os.environ.get("SAN_PREC") == "bf16" else xmgn.PREC_FP16
 for H in (int(a) for a in sys.argv[1:] or ["128", "512"]):
-    pr = Processor(b, H, 2)
+    pr = Processor(b, H, 2, precision=PREC)
     params, io = pr.make_params(), pr.make_io_params()
     gp, gio = torch.zeros(pr.n_params, device="cuda"), torch.zeros_like(io)
     loss = torch.zeros(1, device="cuda")
