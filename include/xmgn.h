@@ -104,13 +104,16 @@ void xmgn_free_graph(xmgn_graph* g);
 
 /* ------------------------------------------------------------------ model
  * precision: XMGN_PREC_BF16 -- BF16 tensor-core operands, FP32 accumulate,
- *            FP32 residual streams / LN / SiLU / aggregation (PAPER.md:234 AMP).
+ *            FP32 residual streams / LN / SiLU / aggregation (PAPER.md:234 AMP);
+ *            the node MLP's first GEMM and the pre-projection take 2 x BF16
+ *            (hi + lo) operands in the forward, P is kept in FP16: max|dh| <=
+ *            2e-2 x RMS after 15 layers (north_star).
  *            XMGN_PREC_FP32_CHECK -- every GEMM operand split hi+lo in BF16 and
  *            multiplied as hi*hi + lo*hi + hi*lo (FP32-class products) for the
  *            1e-4 check mode (north_star); H = 128 only.
- *            XMGN_PREC_FP16 -- as BF16 but with FP16 tensor-core operands (same
- *            MMA rate, 3 more mantissa bits); the mode that meets the 2e-2 x RMS
- *            bound at 15 layers.
+ *            XMGN_PREC_FP16 -- FP16 tensor-core operands (same MMA rate, 3 more
+ *            mantissa bits), 16-bit edge stream; the bench's mode (5x inside the
+ *            2e-2 x RMS bound at 15 layers).
  * mlp_hidden_layers m in {1, 2}; hidden H in {128, 256, 512}.                  */
 enum { XMGN_PREC_BF16 = 0, XMGN_PREC_FP32_CHECK = 1, XMGN_PREC_FP16 = 2 };
 typedef struct {

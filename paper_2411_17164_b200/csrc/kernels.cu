@@ -28,6 +28,21 @@ __global__ void k_pack(const float* __restrict__ params, const PackJob* __restri
 }
 
 // ---------------------------------------------------------------- FP32 -> BF16 (hi [+ lo])
+// FP32 -> 2 x BF16 into separate hi / lo tensors (BF16 mode's 2 x BF16 operands)
+__global__ void k_to_bf16x2(const float* __restrict__ in, __nv_bfloat16* __restrict__ hi_out,
+                            __nv_bfloat16* __restrict__ lo_out, long long n8) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n8; t += (long long)gridDim.x * blockDim.x) {
+    const float4 a = reinterpret_cast<const float4*>(in)[2 * t];
+    const float4 b = reinterpret_cast<const float4*>(in)[2 * t + 1];
+    float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) split2<false, true>(v[2 * i], v[2 * i + 1], hi[i], lo[i]);
+    reinterpret_cast<uint4*>(hi_out)[t] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    reinterpret_cast<uint4*>(lo_out)[t] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
 template <bool F16>
 __global__ void k_to_bf16(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, long long lo_off,
                           long long n8) {
@@ -581,6 +596,13 @@ void launch_to_bf16(bool f16, const float* in, __nv_bfloat16* out, long long lo_
   int blocks = (int)std::min<long long>((n8 + 255) / 256, 148 * 16);
   if (f16) k_to_bf16<true><<<blocks, 256, 0, st>>>(in, out, lo_off, n8);
   else k_to_bf16<false><<<blocks, 256, 0, st>>>(in, out, lo_off, n8);
+}
+void launch_to_bf16x2(const float* in, __nv_bfloat16* hi, __nv_bfloat16* lo, long long n, cudaStream_t st) {
+  if (n <= 0) return;
+  count_launch();
+  long long n8 = n / 8;
+  int blocks = (int)std::min<long long>((n8 + 255) / 256, 148 * 16);
+  k_to_bf16x2<<<blocks, 256, 0, st>>>(in, hi, lo, n8);
 }
 void launch_to_f32(bool f16, const __nv_bfloat16* in, long long lo_off, float* out, long long n, cudaStream_t st,
                    const float* inv) {

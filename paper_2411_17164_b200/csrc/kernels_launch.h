@@ -20,6 +20,7 @@ void launch_to_f32(bool f16, const __nv_bfloat16* in, long long lo_off, float* o
 // backward loss scaling: scale = {S, 1/S} with S = 2^k putting max|g| in [1, 2); out = S g
 void launch_seed_scale(const float* g, long long n, unsigned int* amax_bits, float* out, float* scale, cudaStream_t st);
 void launch_scale_copy(const float* in, long long n, const float* inv, float* out, cudaStream_t st);
+void launch_to_bf16x2(const float* in, __nv_bfloat16* hi, __nv_bfloat16* lo, long long n, cudaStream_t st);
 void launch_to_bf16(bool f16, const float* in, __nv_bfloat16* out, long long lo_off, long long n, cudaStream_t st);
 void launch_aggregate(bool f16, int H, const int* off, const __nv_bfloat16* e, long long e_lo, __nv_bfloat16* a,
                       long long lo_off, int n, cudaStream_t st);

@@ -590,7 +590,7 @@ static void proc_fwd(xmgn_workspace* ws, int part, const float* params, const fl
       launch_to_bf16(ws->f16, e0, ws->e_ck.p, ws->e_ck.lo, e1 * H, st);
     }
     if (ws->bsplit)   // h^0 = hi + lo (hi rewritten with the same RNE bits)
-      launch_to_bf16(false, h0, ws->h_ck.p, (long long)(ws->hlo[0] - ws->h_ck.p), n0 * H, st);
+      launch_to_bf16x2(h0, ws->h_ck.p, ws->hlo[0], n0 * H, st);
     const int W1 = 0, W2 = 2;  // weight map slots
     auto r1 = [&](int l, int slot) { return (l * ws->S1 + slot) * H; };
     auto r2 = [&](int l, int slot) { return (l * ws->S2 + slot) * H; };
