@@ -199,7 +199,7 @@ def test_mse_scaled_upstream_gradient(prec):
     _check(res, ref, 128, 15, TAU[prec], tau_row=TAU_ROW[prec])
 
 
-@pytest.mark.parametrize("prec", [FP32, FP16])
+@pytest.mark.parametrize("prec", [FP32, FP16, BF16])
 def test_zero_variance_layernorm_rows(prec):
     """with the last Linear of layer 1's edge and node MLPs set to
     W = 0 and b = 0.25 (constant), every LayerNorm input row is constant: variance 0,
