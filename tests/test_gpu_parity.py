@@ -283,8 +283,8 @@ def _junction_probes(b, n_per_owner=4, seed=1):
 
 @pytest.mark.slow
 def test_cfg4_probe_forward():
-    """CFG4 (the bench workload: 2M-point 3-level cloud, 8 partitions, H=512, L=15, FP16,
-    the bench's launch configuration): 32 owned probe rows on the borders where four
+    """CFG4 (the bench workload: 2M-point 3-level cloud, 8 partitions, H=512, L=15, FP16 and
+    BF16, the bench's launch configuration): 32 owned probe rows on the borders where four
     partitions meet (two junctions: partitions 0-3 and 4-7), each vs the FP64 oracle on
     the probes' 15-hop ball (itself a halo partition owning the probes).
     Tolerance: 2e-2 x RMS of the oracle's own h^L over the probe rows."""
@@ -294,21 +294,22 @@ def test_cfg4_probe_forward():
     clusters = _junction_probes(b)
     probes = np.concatenate(clusters)
     assert len(probes) >= 32 and len(set(b["owner"][probes])) == 8, (len(probes), set(b["owner"][probes]))
-    res = run_gpu(b, 512, 15, FP16, want_inputs=False)
     P = tensors.params(512, 15).double().numpy()
-    got, ref = [], []
+    ref, rows = [], []
     for c in clusters:
         lg = oracle.local_graph(b["offsets"], b["sources"], c, 15)
         h0 = tensors.node_features(lg["gid"], 512).double().numpy()
         e0 = tensors.edge_features(lg["edge_gid"], 512).double().numpy()
         f = oracle.forward(lg["offsets"], lg["sources"], P, h0, e0, 512, 15)
         ref.append(f["h"][-1][:lg["n_owned"]])
-        got.append(res["h"][lg["gid"][:lg["n_owned"]]])
-    got, ref = np.concatenate(got), np.concatenate(ref)
+        rows.append(lg["gid"][:lg["n_owned"]])
+    ref, rows = np.concatenate(ref), np.concatenate(rows)
     rms = np.sqrt((ref ** 2).mean())
-    err = np.abs(got - ref).max(axis=1) / rms
-    print(f"CFG4 {len(err)} probes: max/RMS worst {err.max():.3e} median {np.median(err):.3e}")
-    assert err.max() <= TAU[FP16], err
+    for prec in (FP16, BF16):   # the bench's mode and north_star's BF16 operands
+        res = run_gpu(b, 512, 15, prec, want_inputs=False)
+        err = np.abs(res["h"][rows] - ref).max(axis=1) / rms
+        print(f"CFG4 prec={prec} {len(err)} probes: max/RMS worst {err.max():.3e} median {np.median(err):.3e}")
+        assert err.max() <= TAU[prec], (prec, err)
 
 
 @pytest.mark.parametrize("prec", [FP16, BF16])
