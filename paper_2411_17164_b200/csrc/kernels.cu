@@ -493,13 +493,16 @@ __global__ void __launch_bounds__(128, (WgradShape<NT, SPLIT>::MINB)) k_wgrad(co
 
 // grad[i] += unscale * sum_{s < S} part[s][i] for i < n, split stride `ld` (fixed order);
 // unscale = inv[0] (the backward's power-of-two loss-scale inverse, exact) or 1
+// (entries i >= n1 go to grad2[i - n1]: the bias columns of a wgrad in the same launch)
 __global__ void k_reduce_part(const float* __restrict__ part, int S, long long n, long long ld,
-                              float* __restrict__ grad, const float* __restrict__ inv) {
+                              float* __restrict__ grad, const float* __restrict__ inv, long long n1,
+                              float* __restrict__ grad2) {
   const float u = inv ? *inv : 1.0f;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int k = 0; k < S; ++k) s += part[k * ld + i];
-    grad[i] += s * u;
+    if (i < n1) grad[i] += s * u;
+    else grad2[i - n1] += s * u;
   }
 }
 
@@ -692,10 +695,10 @@ void launch_wgrad(const WgradParams& p, bool split, bool f16, cudaStream_t st) {
   }
 }
 void launch_reduce_part(const float* part, int S, long long n, long long ld, float* grad, cudaStream_t st,
-                        const float* inv) {
+                        const float* inv, long long n1, float* grad2) {
   count_launch();
   int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
-  k_reduce_part<<<blocks, 256, 0, st>>>(part, S, n, ld, grad, inv);
+  k_reduce_part<<<blocks, 256, 0, st>>>(part, S, n, ld, grad, inv, n1 < 0 ? n : n1, grad2);
 }
 void launch_reduce_colsum(const float* part, int nct, const int* slot, int H, ColsumDst d, float* tmp, float* grad,
                           cudaStream_t st, const float* inv) {

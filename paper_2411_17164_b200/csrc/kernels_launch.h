@@ -31,7 +31,7 @@ void launch_segsum(bool f16, int H, const int* off, const int* rev, const __nv_b
                    __nv_bfloat16* D, long long d_lo, int n, int e_act, cudaStream_t st);
 void launch_wgrad(const WgradParams& p, bool split, bool f16, cudaStream_t st);
 void launch_reduce_part(const float* part, int S, long long n, long long ld, float* grad, cudaStream_t st,
-                        const float* inv = nullptr);
+                        const float* inv, long long n1 = -1, float* grad2 = nullptr);
 constexpr int CS_SEG = 64;   // first-level segments of the column-sum reduce
 // grad[d.off[v] + c] += inv * sum over CTA tiles t < nct and quadrants of part[slot[v]][t][q][c]
 void launch_reduce_colsum(const float* part, int nct, const int* slot, int H, ColsumDst d, float* tmp, float* grad,

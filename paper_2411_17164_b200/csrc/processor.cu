@@ -390,8 +390,12 @@ static void wgrad(xmgn_workspace* ws, const BfBuf& a0, const BfBuf& a1, int a_wi
   XMGN_CUDA(cudaGetLastError(), "wgrad launch");
   const long long ld = (long long)(Hin + (p.ones_tile ? 128 : 0)) * H;
   if (!inv) inv = ws->d_scale + 1;
-  if (Hin > 0) launch_reduce_part(ws->part, S, (long long)Hin * H, ld, grad + dst, st, inv);
-  if (p.ones_tile) launch_reduce_part(ws->part + (long long)Hin * H, S, H, ld, grad + bias_dst, st, inv);
+  // weight and bias partials are contiguous per split: one fixed-order reduce launch for both
+  if (Hin > 0 && p.ones_tile)
+    launch_reduce_part(ws->part, S, (long long)Hin * H + H, ld, grad + dst, st, inv, (long long)Hin * H,
+                       grad + bias_dst);
+  else if (Hin > 0) launch_reduce_part(ws->part, S, (long long)Hin * H, ld, grad + dst, st, inv);
+  else if (p.ones_tile) launch_reduce_part(ws->part + (long long)Hin * H, S, H, ld, grad + bias_dst, st, inv);
 }
 
 // grad[off[v] + c] += (1/S) sum over the last backward launch's tiles and quadrants of vector v
