@@ -223,6 +223,8 @@ struct ChainCfg {
   static constexpr uint32_t TMEM_COLS = H;
   static_assert(SB >= 2, "B ring too small");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+  static_assert(EpiShape<H, SPLIT>::MINB * (SMEM_BYTES + 1024u) <= 228u * 1024u,
+                "the resident CTAs per SM (MINB) must fit the SM's shared memory");
 };
 
 __device__ __forceinline__ float sigmoid_fast(float v) {
