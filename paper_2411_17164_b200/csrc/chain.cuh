@@ -59,8 +59,11 @@ enum : int {
   EF_NO_GA = 131072,   // EPI_LN_BWD + EF_G16: dY = G rows only (no G_a[dst] term, no write-back)
   EF_OUT_HALF = 262144,  // EPI_STORE + EF_OUT16 (16-bit modes): write FP16 whatever the operand type
                          // (the node pre-projections P are epilogue addends, not MMA operands)
-  EF_STORE_LO = 524288   // EPI_LN_FWD (16-bit modes): also write lo = y - rnd16(y) to lo_out (2 x 16-bit
+  EF_STORE_LO = 524288,  // EPI_LN_FWD (16-bit modes): also write lo = y - rnd16(y) to lo_out (2 x 16-bit
                          // GEMM operands of the BF16 mode)
+  EF_ST_SAVE = 1048576,  // EPI_LN_FWD (16-bit modes): write the row's (mean, rstd) to ln_st[row]
+  EF_ST_LOAD = 2097152   // EPI_LN_BWD (16-bit modes): read (mean, rstd) from ln_st[row] (the forward's,
+                         // bitwise those the recompute would give) instead of a statistics pass
 };
 
 enum : int {
@@ -95,6 +98,7 @@ struct Step {
   long long g16_lo;
   __nv_bfloat16* g16_out;         // EPI_ADD + EF_G16 output (same lo offset as g16)
   __nv_bfloat16* lo_out;          // EPI_LN_FWD + EF_STORE_LO: lo rows [rows][H]
+  float2* ln_st;                  // EF_ST_SAVE / EF_ST_LOAD: per-row LayerNorm (mean, rstd) [rows]
   const __nv_bfloat16* ga16;      // 16-bit aggregation adjoint G_a [N][H] gathered by dst (EF_G16)
   long long ga16_lo;
   // 16-bit modes: the epilogue's contiguous 16-bit row input (S', G_e, G_e', residual) is

@@ -375,6 +375,7 @@ __device__ __forceinline__ void op_ln_fwd(const Epi& e, const Step& st, Wait wai
   wait();
   float mean, rstd;
   ln_stats16<H, NC>(e, e.eps, row_sum, mean, rstd);
+  if ((st.flags & EF_ST_SAVE) && e.valid && e.cb == 0) st.ln_st[e.r] = make_float2(mean, rstd);
   uint32_t ta[16];
   tmem_ld16_async(e.tl, ta);
   auto body = [&](int cc, uint32_t* q) {
@@ -440,9 +441,14 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
   const bool tin = st.in_map >= 0;   // G_e rows arrive in ACT by TMA (rows >= valid_in read zero)
   if (has_g && !tin) { ld16(gp16, g0); ld16(gp16 + 16, g1); }
   if (ga) { ld16(ap16, a0); ld16(ap16 + 16, a1); }
+  // the forward's statistics (EF_ST_LOAD): issued before the accumulator wait; rows >= M
+  // (no forward row) take finite dummies, their dY is 0
+  const bool ldst = (st.flags & EF_ST_LOAD) != 0;
+  float2 ms = make_float2(0.f, 1.f);
+  if (ldst && e.valid) ms = __ldg(st.ln_st + e.r);
   wait();
-  float mean, rstd;
-  ln_stats16<H, NC>(e, e.eps, row_sum, mean, rstd);
+  float mean = ms.x, rstd = ms.y;
+  if (!ldst) ln_stats16<H, NC>(e, e.eps, row_sum, mean, rstd);
   float s1 = 0.f, s2 = 0.f;
   uint32_t ta[16];
   tmem_ld16_async(e.tl, ta);
@@ -523,9 +529,14 @@ __device__ __forceinline__ void op_ln_bwd32(const Epi& e, const Step& st, Wait w
 #pragma unroll
   for (int i = 0; i < 16; ++i) g0[i] = 0u;
   if (has_g) ld32x16(gp32, g0);
+  // the forward's statistics (EF_ST_LOAD): issued before the accumulator wait; rows >= M
+  // (no forward row) take finite dummies, their dY is 0
+  const bool ldst = (st.flags & EF_ST_LOAD) != 0;
+  float2 ms = make_float2(0.f, 1.f);
+  if (ldst && e.valid) ms = __ldg(st.ln_st + e.r);
   wait();
-  float mean, rstd;
-  ln_stats16<H, NC>(e, e.eps, row_sum, mean, rstd);
+  float mean = ms.x, rstd = ms.y;
+  if (!ldst) ln_stats16<H, NC>(e, e.eps, row_sum, mean, rstd);
   float s1 = 0.f, s2 = 0.f;
   uint32_t ta[16];
   tmem_ld16_async(e.tl, ta);

@@ -64,6 +64,11 @@ struct xmgn_workspace {
   xmgn::BfBuf wkx;                // [L][3][H][4H]: [W0h^T W0a^T W0h^T W0a^T]; [W0s^T W0s^T]; [W0d^T W0d^T]
   xmgn::bf16* hlo[2] = {nullptr, nullptr};  // lo halves of h^l (ping-pong by l)
   xmgn::bf16* alo = nullptr;      // lo half of a^l
+  // per-row LayerNorm (mean, rstd) of every layer's edge / node update, written by the forward
+  // and read by the backward instead of a statistics pass (16-bit training modes;
+  // XMGN_LN_STATS=0: off)
+  float2* lnst_e = nullptr;       // [L][Emax]
+  float2* lnst_n = nullptr;       // [L][Nmax]
   xmgn::BfBuf P;                  // node pre-projections, one per layer [L][Nmax][2H], 16-bit (kept for the bwd)
   // backward
   float* Gh = nullptr;            // dL/dh (FP32, node level)
@@ -510,6 +515,13 @@ static xmgn_status workspace_create(const xmgn_graph* g, const xmgn_model_cfg* c
       ws->e32_mode = cfg->precision == XMGN_PREC_BF16;
       if (ws->e32_mode)
         for (int i = 0; i < 2; ++i) ws->e32[i] = (float*)dalloc(ws, EH * 4);
+      {
+        const char* le = getenv("XMGN_LN_STATS");
+        if (!infer && !ws->split && !(le && atoi(le) == 0)) {
+          ws->lnst_e = (float2*)dalloc(ws, (size_t)L * ws->Emax * sizeof(float2));
+          ws->lnst_n = (float2*)dalloc(ws, (size_t)L * ws->Nmax * sizeof(float2));
+        }
+      }
       if (ws->bsplit) {
         for (int i = 0; i < 2; ++i) ws->hlo[i] = (bf16*)dalloc(ws, NH * 2);
         ws->alo = (bf16*)dalloc(ws, NH * 2);
@@ -661,6 +673,7 @@ static void proc_fwd(xmgn_workspace* ws, int part, const float* params, const fl
           if (!ws->split && el > 0) s.in_map = pr.in_map(eck_prev.p, el, H);   // residual e^{l-1} rows
         }
         s.bf_out = eck_next.p; s.bf_lo = eck_next.lo;
+        if (ws->lnst_e) { s.flags |= EF_ST_SAVE; s.ln_st = ws->lnst_e + (long long)li * ws->Emax; }
         run_prog(ws, "chain_edge_fwd", pr, (int)el, dp.src, dp.dst, false, st);
       }
       // aggregation (Eq. 2) -> a^l (BF16 operand + checkpoint)
@@ -692,6 +705,7 @@ static void proc_fwd(xmgn_workspace* ws, int part, const float* params, const fl
         s.gamma = params + Ly.gamma(li, 1); s.beta = params + Ly.beta(li, 1);
         s.f_in = h_in; s.ld_in = H; s.f_out = hn; s.ld_out = H;
         s.flags = EF_STORE_F32;
+        if (ws->lnst_n) { s.flags |= EF_ST_SAVE; s.ln_st = ws->lnst_n + (long long)li * ws->Nmax; }
         if (l == L && hL16) {
           s.flags |= EF_STORE_BF;
           s.bf_out = hL16; s.bf_lo = 0;
@@ -798,6 +812,8 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         s.a_src = A_ACT; s.K = H; s.b_map = W1; s.b_row0 = r1(li, (blk ? sl_njt(m) : SL_EJT) + m - 1);
         s.epi = EPI_LN_BWD; s.bias = params + Ly.b(li, blk, m);
         if (blk == 1) s.flags |= EF_COLSUM_ALL;
+        if (blk == 0 && ws->lnst_e) { s.flags |= EF_ST_LOAD; s.ln_st = ws->lnst_e + (long long)li * ws->Emax; }
+        if (blk == 1 && ws->lnst_n) { s.flags |= EF_ST_LOAD; s.ln_st = ws->lnst_n + (long long)li * ws->Nmax; }
         s.gamma = params + Ly.gamma(li, blk); s.beta = params + Ly.beta(li, blk);
         s.f_in = ws->Gh; s.ld_in = H;
         s.valid_in = blk ? (int)nl : (int)enext;
