@@ -407,11 +407,17 @@ namespace xmgn {
 #ifndef XMGN_STATIC_TILES
 #define XMGN_STATIC_TILES 1
 #endif
+// The OPS-specialised edge-forward kernel compiles the dynamic queue in even so (it does not
+// spill there); it runs dynamic when the launch passes a tile counter (XMGN_DYN_FWD=0: static).
+#ifndef XMGN_DYN_EDGE_FWD
+#define XMGN_DYN_EDGE_FWD 1
+#endif
+template <bool DYN>
 struct TileSched {   // everything but the queue base is re-derived at each call (few live registers)
   const ChainParams* p;
   uint64_t* base;        // tq_full[TQ], tq_empty[TQ], then int q[TQ]
   __device__ __forceinline__ int at(int i) const {   // every role
-    if (XMGN_STATIC_TILES || !p->tile_counter) {
+    if (!DYN || !p->tile_counter) {
       const int t = (int)cluster_id_x() + i * (int)n_clusters_x();
       return t < (p->M + 255) / 256 ? t : -1;
     }
@@ -419,7 +425,7 @@ struct TileSched {   // everything but the queue base is re-derived at each call
     return *reinterpret_cast<volatile int*>(reinterpret_cast<int*>(base + 2 * TQ) + i % TQ);
   }
   __device__ __forceinline__ int claim(int i) const {   // the leader's producer (one lane)
-    if (XMGN_STATIC_TILES || !p->tile_counter) return at(i);
+    if (!DYN || !p->tile_counter) return at(i);
     const int slot = i % TQ;
     if (i >= TQ) mbar_wait_cluster(&base[TQ + slot], ((i / TQ) - 1) & 1);
     const int t = atomicAdd(p->tile_counter, 1);
@@ -432,7 +438,7 @@ struct TileSched {   // everything but the queue base is re-derived at each call
     return tile;
   }
   __device__ __forceinline__ void done(int i) const {   // hand-off warps, lane 0, after the tile
-    if (XMGN_STATIC_TILES || !p->tile_counter) return;
+    if (!DYN || !p->tile_counter) return;
     if (cluster_ctarank() == 0) mbar_arrive(&base[TQ + i % TQ]);
     else mbar_arrive_cluster(mapa_shared(smem_u32(&base[TQ + i % TQ]), 0));
   }
@@ -541,7 +547,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<H, SPLIT>::
   // the leader's producer claims pair tiles with an atomic counter and queues them in both
   // CTAs' tq[] (TQ slots); every role reads the same sequence.  A slot is reused only after the
   // hand-off warps of both CTAs finished its tile, by which time every role has read it.
-  const TileSched ts{&p, tq_full};
+  constexpr bool DYN = !XMGN_STATIC_TILES || (XMGN_DYN_EDGE_FWD && PIPE && !BWD && OPS == OPS_EDGE_FWD);
+  const TileSched<DYN> ts{&p, tq_full};
 
   // register split (setmaxnreg, per warpgroup): control warps 0-3 need few registers,
   // the epilogue warpgroups get the rest

@@ -107,6 +107,7 @@ struct xmgn_workspace {
   bool pipe = true;     // N-half-pipelined chain kernel where a program allows it (XMGN_PIPE=0: off)
   bool prm_table = true;  // per-launch static bias/gamma/beta table in the chain kernels (XMGN_PRM_TABLE=0: off)
   bool dyn = false;     // dynamic tile scheduling in the chain kernels (XMGN_DYN=1, needs XMGN_STATIC_TILES=0)
+  bool dyn_fwd = true;  // dynamic tiles in the edge-forward kernel (XMGN_DYN_FWD=0: off)
   int* d_tile_counter = nullptr;
   // checkpoint slot of layer l's tensors (training: one per layer; inference: ping-pong)
   long long ck(int l) const { return infer ? (l & 1) : l; }
@@ -334,8 +335,11 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
     ws->cs_nct = nct;
   }
   const bool pipe = ws->pipe && chain_can_pipe(ws->H, ws->split, p);
-  p.tile_counter = ws->dyn ? ws->d_tile_counter : nullptr;
-  if (ws->dyn) XMGN_CUDA(cudaMemsetAsync(ws->d_tile_counter, 0, sizeof(int), st), "tile counter");
+  // dynamic tiles: every program with XMGN_DYN=1 (needs XMGN_STATIC_TILES=0), and the edge forward
+  // (its kernel compiles the queue in; XMGN_DYN_FWD=0: static)
+  const bool dyn = ws->dyn || (ws->dyn_fwd && !strcmp(name, "chain_edge_fwd"));
+  p.tile_counter = dyn ? ws->d_tile_counter : nullptr;
+  if (dyn) XMGN_CUDA(cudaMemsetAsync(ws->d_tile_counter, 0, sizeof(int), st), "tile counter");
   {
     ProfScope ps(name, st);
     launch_chain(ws->H, ws->split, ws->f16, bwd, p, grid, st, pipe);
@@ -467,6 +471,7 @@ static xmgn_status workspace_create(const xmgn_graph* g, const xmgn_model_cfg* c
       { const char* pe = getenv("XMGN_PIPE"); ws->pipe = !(pe && atoi(pe) == 0); }
       { const char* pt = getenv("XMGN_PRM_TABLE"); ws->prm_table = !(pt && atoi(pt) == 0); }
       { const char* de = getenv("XMGN_DYN"); ws->dyn = de && atoi(de) == 1; }   // see XMGN_STATIC_TILES
+      { const char* df = getenv("XMGN_DYN_FWD"); ws->dyn_fwd = !(df && atoi(df) == 0); }
       ws->dev = g->device;
       ws->H = H; ws->L = L; ws->m = m;
       ws->split = cfg->precision == XMGN_PREC_FP32_CHECK;
