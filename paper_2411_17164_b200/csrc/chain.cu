@@ -25,6 +25,8 @@ static void chain_launch(const ChainParams& p, int grid, cudaStream_t st) {
   kern<<<grid, EpiShape<H, SPLIT>::THREADS, C::SMEM_BYTES, st>>>(p);
 }
 
+bool chain_dyn(int H, bool split) { return XMGN_DYN128 && H == 128 && !split; }
+
 int chain_ctas_per_sm(int H, bool split) {
   if (H == 128) return split ? EpiShape<128, true>::MINB : EpiShape<128, false>::MINB;
   return H == 256 ? EpiShape<256, false>::MINB : EpiShape<512, false>::MINB;

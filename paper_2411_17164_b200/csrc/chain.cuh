@@ -412,6 +412,12 @@ namespace xmgn {
 #ifndef XMGN_DYN_EDGE_FWD
 #define XMGN_DYN_EDGE_FWD 1
 #endif
+// H = 128 (16-bit modes): every chain program on the dynamic queue (balances the 4-CTA/SM grid).
+// Off: the queue's state makes the 96-register H = 128 epilogue spill more -- CFG2 +5%
+// (profiles/r03r_ab_dyn128_rejected.txt)
+#ifndef XMGN_DYN128
+#define XMGN_DYN128 0
+#endif
 template <bool DYN>
 struct TileSched {   // everything but the queue base is re-derived at each call (few live registers)
   const ChainParams* p;
@@ -547,7 +553,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<H, SPLIT>::
   // the leader's producer claims pair tiles with an atomic counter and queues them in both
   // CTAs' tq[] (TQ slots); every role reads the same sequence.  A slot is reused only after the
   // hand-off warps of both CTAs finished its tile, by which time every role has read it.
-  constexpr bool DYN = !XMGN_STATIC_TILES || (XMGN_DYN_EDGE_FWD && PIPE && !BWD && OPS == OPS_EDGE_FWD);
+  constexpr bool DYN = !XMGN_STATIC_TILES || (XMGN_DYN_EDGE_FWD && PIPE && !BWD && OPS == OPS_EDGE_FWD) ||
+                       (XMGN_DYN128 && H == 128 && !SPLIT);
   const TileSched<DYN> ts{&p, tq_full};
 
   // register split (setmaxnreg, per warpgroup): control warps 0-3 need few registers,

@@ -72,6 +72,7 @@ void launch_chain(int H, bool split, bool f16, bool bwd, const ChainParams& p, i
 bool chain_can_pipe(int H, bool split, const ChainParams& p);
 size_t chain_smem(int H, bool split);
 int chain_ctas_per_sm(int H, bool split);
+bool chain_dyn(int H, bool split);        // every program of this H on the dynamic tile queue
 int wgrad_ctas_per_sm(int H, bool split);   // resident k_wgrad CTAs per SM (H = 128: 2)   // resident chain CTAs per SM (H = 128: 2)
 
 }  // namespace xmgn

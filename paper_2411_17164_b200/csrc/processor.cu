@@ -337,7 +337,8 @@ static void run_prog(xmgn_workspace* ws, const char* name, Prog& pr, int M, cons
   const bool pipe = ws->pipe && chain_can_pipe(ws->H, ws->split, p);
   // dynamic tiles: every program with XMGN_DYN=1 (needs XMGN_STATIC_TILES=0), and the edge forward
   // (its kernel compiles the queue in; XMGN_DYN_FWD=0: static)
-  const bool dyn = ws->dyn || (ws->dyn_fwd && !strcmp(name, "chain_edge_fwd"));
+  const bool dyn = ws->dyn || (ws->dyn_fwd && !strcmp(name, "chain_edge_fwd")) ||
+                   (ws->dyn_fwd && chain_dyn(ws->H, ws->split));
   p.tile_counter = dyn ? ws->d_tile_counter : nullptr;
   if (dyn) XMGN_CUDA(cudaMemsetAsync(ws->d_tile_counter, 0, sizeof(int), st), "tile counter");
   {
