@@ -218,11 +218,11 @@ struct ChainCfg {
   static constexpr uint32_t SMEM_LIMIT =
       EpiShape<H, SPLIT>::MINB > 1 ? 228u * 1024u / EpiShape<H, SPLIT>::MINB - 1024u : 227u * 1024u;
   static constexpr uint32_t PRM_BYTES = 2u * 3u * H * 4u;        // per-step bias/gamma/beta, double-buffered
-  static constexpr int SB_FIT = (int)((SMEM_LIMIT - 1536u - 512u * EpiShape<H, SPLIT>::EW - PRM_BYTES - ACT_BYTES) / B_SLOT);
+  static constexpr int SB_FIT = (int)((SMEM_LIMIT - 1536u - 1024u * EpiShape<H, SPLIT>::EW - PRM_BYTES - ACT_BYTES) / B_SLOT);
   static constexpr int SB = SB_FIT > 8 ? 8 : SB_FIT;
   static constexpr uint32_t BAR_OFF = ACT_BYTES + SB * B_SLOT;
-  static constexpr uint32_t RED_OFF = BAR_OFF + 512;             // row-reduction exchange [EW][128] f32
-  static constexpr uint32_t PRM_OFF = RED_OFF + EpiShape<H, SPLIT>::EW * 128 * 4;
+  static constexpr uint32_t RED_OFF = BAR_OFF + 512;             // row-reduction exchange [2][EW][128] f32
+  static constexpr uint32_t PRM_OFF = RED_OFF + 2 * EpiShape<H, SPLIT>::EW * 128 * 4;
   static constexpr uint32_t SMEM_BYTES = PRM_OFF + PRM_BYTES + 1024;  // + alignment slack
   static constexpr uint32_t TMEM_COLS = H;
   static_assert(SB >= 2, "B ring too small");
@@ -844,6 +844,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<H, SPLIT>::
         return t;
       }
     };
+    // two row sums in one exchange (the same per-value order as two row_sum calls: same bits)
+    auto row_sum2 = [&](float& a, float& b) {
+      if constexpr (EW > 1) {
+        red[eg * 128 + trow] = a;
+        red[(EW + eg) * 128 + trow] = b;
+        named_bar(1 + q, 32 * EW);
+        float ta = red[trow], tb = red[EW * 128 + trow];
+#pragma unroll
+        for (int j = 1; j < EW; ++j) {
+          ta += red[j * 128 + trow];
+          tb += red[(EW + j) * 128 + trow];
+        }
+        named_bar(1 + q, 32 * EW);
+        a = ta;
+        b = tb;
+      }
+    };
     // per-(CTA tile, quadrant) column-sum partials in global memory: lane l of this warp owns
     // column c0 + l of every chunk; each entry is written exactly once per launch (by the one
     // warp that runs that tile and quadrant), so the partials do not depend on the CTA <-> tile
@@ -1245,12 +1262,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiShape<H, SPLIT>::
           } else if constexpr (BWD) {
             if (ob == OPB_LNB16) {
               if constexpr ((OPS & OPB_LNB16) != 0) {
-                op_ln_bwd16<H, NC16, F16>(e, st, wait, row_sum);
+                op_ln_bwd16<H, NC16, F16>(e, st, wait, row_sum, row_sum2);
                 wrote_act = true;
               }
             } else if (ob == OPB_LNB32) {
               if constexpr ((OPS & OPB_LNB32) != 0) {
-                op_ln_bwd32<H, NC16, F16>(e, st, wait, row_sum);
+                op_ln_bwd32<H, NC16, F16>(e, st, wait, row_sum, row_sum2);
                 wrote_act = true;
               }
             } else if (ob == OPB_DSILU) {

@@ -12,6 +12,9 @@
 // over the warp followed by a fixed-order read-modify-write of per-(CTA,
 // quadrant) global partials, so results are bitwise run-to-run stable.
 #pragma once
+#ifndef XMGN_ROWSUM2
+#define XMGN_ROWSUM2 1
+#endif
 #include "tc.cuh"
 
 
@@ -427,8 +430,8 @@ __device__ __forceinline__ void op_ln_fwd(const Epi& e, const Step& st, Wait wai
 // back (16-bit) as G_e'; LayerNorm backward dz = rstd (dY*g - mean(dY*g) - x^ mean(dY*g x^))
 // -> ACT + scratch dZ; dgamma (and with EF_COLSUM_ALL dbeta, db) column sums.
 // Pass A stashes the rounded dY in ACT at the position pass B overwrites with dz.
-template <int H, int NC, bool F16, class Wait, class RowSum>
-__device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait wait, RowSum row_sum) {
+template <int H, int NC, bool F16, class Wait, class RowSum, class RowSum2>
+__device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait wait, RowSum row_sum, RowSum2 row_sum2) {
   const bool csall = (st.flags & EF_COLSUM_ALL) != 0;
   const bool has_g = e.valid && e.r < st.valid_in;
   const bool ga = e.valid && !(st.flags & EF_NO_GA);   // G_a[dst] term + G_e' write-back
@@ -495,8 +498,15 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
     passA(cc, g0, a0);
     passA(cc + 1, g1, a1);
   }
+#if XMGN_ROWSUM2
+  row_sum2(s1, s2);                                  // one exchange for both sums (same bits)
+  s1 *= (1.0f / H);
+  s2 *= (1.0f / H);
+#else
+  (void)row_sum2;
   s1 = row_sum(s1) * (1.0f / H);
   s2 = row_sum(s2) * (1.0f / H);
+#endif
   tmem_ld16_async(e.tl, ta);
 #pragma unroll 1
   for (int cc = 0; cc < NC; ++cc) {
@@ -519,8 +529,8 @@ __device__ __forceinline__ void op_ln_bwd16(const Epi& e, const Step& st, Wait w
 }
 
 // EPI_LN_BWD, node form: dY = G_h rows (FP32 f_in, rows < valid_in); same math.
-template <int H, int NC, bool F16, class Wait, class RowSum>
-__device__ __forceinline__ void op_ln_bwd32(const Epi& e, const Step& st, Wait wait, RowSum row_sum) {
+template <int H, int NC, bool F16, class Wait, class RowSum, class RowSum2>
+__device__ __forceinline__ void op_ln_bwd32(const Epi& e, const Step& st, Wait wait, RowSum row_sum, RowSum2 row_sum2) {
   const bool csall = (st.flags & EF_COLSUM_ALL) != 0;
   const bool has_g = e.valid && e.r < st.valid_in;
   const float* gp32 = st.f_in + (size_t)e.r * st.ld_in + e.cb;
@@ -572,8 +582,15 @@ __device__ __forceinline__ void op_ln_bwd32(const Epi& e, const Step& st, Wait w
     passA(cc, g0);
     passA(cc + 1, g0);
   }
+#if XMGN_ROWSUM2
+  row_sum2(s1, s2);                                  // one exchange for both sums (same bits)
+  s1 *= (1.0f / H);
+  s2 *= (1.0f / H);
+#else
+  (void)row_sum2;
   s1 = row_sum(s1) * (1.0f / H);
   s2 = row_sum(s2) * (1.0f / H);
+#endif
   if (has_g) ld32x16(gp32, g0);
   tmem_ld16_async(e.tl, ta);
   auto passB = [&](int cc, uint32_t* gq) {
