@@ -106,7 +106,9 @@ struct xmgn_workspace {
   bool infer = false;   // inference workspace: forward only, per-layer buffers ping-ponged
   bool pipe = true;     // N-half-pipelined chain kernel where a program allows it (XMGN_PIPE=0: off)
   bool prm_table = true;  // per-launch static bias/gamma/beta table in the chain kernels (XMGN_PRM_TABLE=0: off)
-  bool db0_node = true;   // edge db_0 from the node-level D_dst column sums (XMGN_DB0_NODE=0: from dZ0 rows)
+  // edge db_0 from the node-level D_dst column sums (XMGN_DB0_NODE=1).  Off by default: CFG4 -0.8%,
+  // but the BF16 CFG2 run hung with it (profiles/r03k_db0_node_hang.txt; root cause not found)
+  bool db0_node = false;
   bool dyn = false;     // dynamic tile scheduling in the chain kernels (XMGN_DYN=1, needs XMGN_STATIC_TILES=0)
   bool dyn_fwd = true;  // dynamic tiles in the edge-forward kernel (XMGN_DYN_FWD=0: off)
   int* d_tile_counter = nullptr;
@@ -472,7 +474,7 @@ static xmgn_status workspace_create(const xmgn_graph* g, const xmgn_model_cfg* c
       ws->infer = infer;
       { const char* pe = getenv("XMGN_PIPE"); ws->pipe = !(pe && atoi(pe) == 0); }
       { const char* pt = getenv("XMGN_PRM_TABLE"); ws->prm_table = !(pt && atoi(pt) == 0); }
-      { const char* db = getenv("XMGN_DB0_NODE"); ws->db0_node = !(db && atoi(db) == 0); }
+      { const char* db = getenv("XMGN_DB0_NODE"); ws->db0_node = db && atoi(db) == 1; }
       { const char* de = getenv("XMGN_DYN"); ws->dyn = de && atoi(de) == 1; }   // see XMGN_STATIC_TILES
       { const char* df = getenv("XMGN_DYN_FWD"); ws->dyn_fwd = !(df && atoi(df) == 0); }
       ws->dev = g->device;
@@ -873,7 +875,7 @@ extern "C" xmgn_status xmgn_processor_bwd(xmgn_workspace* ws, int part, const fl
         colsum_reduce(ws, 0, li, grad_params, chain_grid(ws, (int)el), st, /*gamma_only=*/true);
         // bias gradients ride on the weight-gradient GEMMs (all-ones A tile); dbeta = sum_rows G_e';
         // db_0 = sum_rows dZ0 = sum over nodes of D_dst (every active edge has one destination) rides
-        // on the node-level dW_d wgrad below (XMGN_DB0_NODE=0: on this edge-level wgrad)
+        // on the node-level dW_d wgrad below when XMGN_DB0_NODE=1 (default: this edge-level wgrad)
         wgrad(ws, eck, none, H, H / 128, ws->scrZ[0], H, 0, el, H, grad_params, Ly.W(li, 0, 0), st,
               ws->db0_node ? -1 : Ly.b(li, 0, 0));
         for (int j = 1; j <= m; ++j)
